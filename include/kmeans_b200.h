@@ -1,0 +1,158 @@
+/*
+ * kmeans_b200.h — C ABI of the B200-native MTI-pruned Lloyd's k-means hot path.
+ *
+ * Method: Lloyd's k-means (§4.1) with Minimal Triangle
+ * Inequality pruning (§3.3), merged MM step with per-thread
+ * state and one reduction per iteration (§3.2) and the
+ * distributed "merge global state" step (§7) realised as one
+ * NCCL allreduce per iteration.  Readings of garbled/silent passages: DESIGN.md "Readings".
+ *
+ * One iteration t (kmeans_iterate) runs, on the context's CUDA stream:
+ *   S1 geometry + drift  f(c) = ||C_t-1[c] - C_t-2[c]||, H = 1/2 ||C[c]-C[c']||,
+ *                        s(c) = min_{c'!=c} H, neighbour lists sorted by H
+ *   S2 MTI assignment    u += f(a); skip point iff u <= s(a); else tighten u = d(x, C[a]) and
+ *                        skip candidate c' iff H[a][c'] >= u
+ *   S3 reduction         per-cluster fp64 sums and counts, allreduced over ranks
+ *   S4 update            C_t[c] = sum/count, or C_t-1[c] when the cluster is empty; stop iff changed <= tol
+ * Iteration 1 has no bounds: every point evaluates all k centroids (S0).
+ *
+ * Precision ("exact mode"): fp32 points and fp32 screening distances with
+ * rigorously rounded bounds derived from the fp64 master centroids; candidates whose fp32
+ * error intervals overlap are re-evaluated in fp64, so assignments equal the fp64 argmin;
+ * sums, counts and centroids are fp64.
+ *
+ * Conventions for every call:
+ *   - returns km_status; KM_OK (0) on success.  On failure a thread-local message is
+ *     available from kmeans_last_error() and the context is left unchanged unless stated.
+ *   - a context is used by one host thread at a time; many contexts per process are allowed.
+ *   - all work is enqueued on the context stream; calls that return host values synchronise it.
+ */
+#ifndef KMEANS_B200_H
+#define KMEANS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t km_status;
+enum {
+    KM_OK = 0,
+    KM_EARG = 1,        /* invalid argument (sizes, null or misaligned pointers, k > n_global, d > 64, k > 4096) */
+    KM_ENONFINITE = 2,  /* NaN/Inf found in points or centroids (only when check_finite = 1) */
+    KM_ECUDA = 3,       /* CUDA runtime error (message has cudaGetErrorString) */
+    KM_ENCCL = 4,       /* NCCL error, or libnccl.so.2 could not be loaded for world > 1 */
+    KM_ENOMEM = 5,      /* device allocation failed */
+    KM_ESTATE = 6       /* call not valid in the current state (e.g. sse before any iteration) */
+};
+
+enum { KM_PRUNE_MTI = 0, KM_PRUNE_NONE = 1 };
+
+/* Row re-bucketing policy: the context keeps its own copy of
+ * the points physically sorted by (assigned cluster, survivor-prefix class) so that warps
+ * evaluate candidates with broadcast centroid reads.  AUTO re-sorts after iteration 1 and
+ * whenever the points reassigned since the last sort exceed resort_fraction * n_local. */
+enum { KM_RESORT_AUTO = 0, KM_RESORT_NEVER = 1, KM_RESORT_ALWAYS = 2 };
+
+typedef struct km_options {
+    int32_t device;            /* CUDA device ordinal the context lives on */
+    void *stream;              /* cudaStream_t, borrowed; NULL = the context creates its own */
+    int32_t prune;             /* KM_PRUNE_MTI (knori) or KM_PRUNE_NONE (knori-, all k distances) */
+    int32_t rank;              /* this process's rank, 0 <= rank < world */
+    int32_t world;             /* number of ranks (GPUs); 1 = no collective */
+    uint8_t nccl_unique_id[128]; /* ncclUniqueId from kmeans_nccl_unique_id() on rank 0 (world > 1) */
+    int64_t n_global;          /* total rows over all ranks (used for k <= n_global); 0 = n_local * world */
+    int32_t check_finite;      /* 1 = scan points and centroids for NaN/Inf at create (KM_ENONFINITE) */
+    int32_t points_on_host;    /* 1 = points pointer is host memory (pinned preferred); copied at create */
+    int32_t resort_policy;     /* KM_RESORT_* */
+    float resort_fraction;     /* AUTO threshold, default 0.10 */
+    int32_t reserved[8];
+} km_options;
+
+typedef struct km_iter_stats {
+    int64_t changed;   /* points whose assignment changed (global, post-allreduce); iteration 1: n */
+    int64_t dists;     /* point-centroid distances evaluated under the MTI semantics (global) */
+    int64_t clause1;   /* points skipped by clause 1 (global) */
+    int64_t refined;   /* points re-evaluated in fp64 by exact mode (global) */
+    int32_t empty;     /* clusters with no points after this iteration's assignment */
+    int32_t resorted;  /* 1 if the rows were re-bucketed after this iteration's pass */
+    float ms_iter;     /* device time of the whole iteration (CUDA events, this rank) */
+    float ms_assign;   /* device time of the assignment(+reduction) kernel (this rank) */
+    float ms_sort;     /* device time of re-bucketing (0 if none) */
+    float ms_comm;     /* device time of the allreduce (0 if world == 1) */
+} km_iter_stats;
+
+typedef struct km_ctx km_ctx;
+
+/* Fill *opt with defaults: device 0, NULL stream, MTI, rank 0, world 1, AUTO re-sort at 0.10. */
+void kmeans_default_options(km_options *opt);
+
+/* rank 0 only (world > 1): write a fresh ncclUniqueId (128 bytes) to out; the caller
+ * broadcasts it to the other ranks and passes it in km_options.nccl_unique_id.  Loads
+ * libnccl.so.2 dynamically (KM_ENCCL if unavailable). */
+km_status kmeans_nccl_unique_id(uint8_t out[128]);
+
+/*
+ * Create a context for this rank's shard.
+ *   n_local           rows held by this rank (>= 1); rank r of G conventionally holds rows
+ *                     [floor(r n/G), floor((r+1) n/G)) of the global data
+ *   d                 dimensions, 1 <= d <= 64
+ *   k                 clusters, 1 <= k <= min(4096, n_global)
+ *   points            n_local x d fp32, row-major, contiguous.  Device memory on opt->device
+ *                     (borrowed: read during create only, never written) or host memory when
+ *                     opt->points_on_host = 1.  Must be 4-byte aligned.
+ *   init_centroids    k x d fp64 row-major host array (copied); identical on all ranks.
+ *   opt               may be NULL (defaults).  Ownership of opt->stream stays with the caller.
+ *   out               receives the context.
+ * Collective over ranks when world > 1 (NCCL communicator creation).
+ * Errors: KM_EARG, KM_ENONFINITE, KM_ECUDA, KM_ENCCL, KM_ENOMEM.
+ */
+km_status kmeans_create(int64_t n_local, int32_t d, int32_t k, const float *points,
+                        const double *init_centroids, const km_options *opt, km_ctx **out);
+
+/* One full iteration (S1-S4; S0 on the first call).  Collective when world > 1.
+ * changed / dists (may be NULL) receive this iteration's global counts. */
+km_status kmeans_iterate(km_ctx *ctx, int64_t *changed, int64_t *dists);
+
+/* Iterate until changed <= tol (a count of points; BASELINE uses tol = 0) or max_iters
+ * iterations have run in this call.  max_iters = 0 runs nothing (iterations = 0, centroids
+ * unchanged).  iterations / dists_total (may be NULL) receive this call's totals. */
+km_status kmeans_run(km_ctx *ctx, int32_t max_iters, int64_t tol, int32_t *iterations,
+                     int64_t *dists_total);
+
+/* n_local int32 assignments of the last assignment pass, in the caller's row order
+ * (reading A9: not re-argmin against the final centroids).  out is host memory unless
+ * out_is_device = 1 (device memory on the context device).  KM_ESTATE before iteration 1. */
+km_status kmeans_get_assignments(km_ctx *ctx, int32_t *out, int32_t out_is_device);
+
+/* k x d fp64 current centroids C_T (host memory, caller-owned).  Identical on all ranks. */
+km_status kmeans_get_centroids(km_ctx *ctx, double *out_host);
+
+/* Replace the current centroids (k x d fp64 host).  The next iteration computes drift
+ * against the centroids the last pass used, so the kept bounds stay sound (lockstep parity). */
+km_status kmeans_set_centroids(km_ctx *ctx, const double *centroids_host);
+
+/* Global SSE = sum_i ||x_i - C_T[a_T(i)]||^2 in fp64 (S5; Eq. 1 read as SSE).  Collective
+ * when world > 1.  KM_ESTATE before iteration 1. */
+km_status kmeans_sse(km_ctx *ctx, double *out);
+
+/* Copy up to cap per-iteration records (oldest first); *count = records available. */
+km_status kmeans_get_stats(km_ctx *ctx, km_iter_stats *out, int32_t cap, int32_t *count);
+
+/* Number of kernel launches this context has issued so far (for launch accounting). */
+int64_t kmeans_launch_count(const km_ctx *ctx);
+
+/* Release all device memory, the internal stream (if created) and the NCCL communicator. */
+void kmeans_destroy(km_ctx *ctx);
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+const char *kmeans_last_error(void);
+
+/* Library version string. */
+const char *kmeans_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMEANS_B200_H */

@@ -1,0 +1,615 @@
+// km_api.cu — C-ABI runtime for the B200-native MTI k-means hot path (include/kmeans_b200.h).
+//
+// Host side of one iteration, all on the context stream:
+//   [re-bucket rows]           if AUTO and rows reassigned since the last sort > fraction * n
+//   k_prep                     S1 geometry/drift
+//   k_assign                   S2+S3 fused; iteration 1: dense
+//                              pass, re-bucket, reduction pass (S0)
+//   ncclAllReduce (world > 1)  one fp64 sum of [sums | counts] + one int64 sum of the counters
+//                              ("merge global state")
+//   k_update                   S4; then one D2H of the counters and a stream sync for the stop test
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only; the library is loaded with dlopen when world > 1
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kmeans_b200.h"
+#include "km_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+km_status fail(km_status s, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define KM_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(e_ == cudaErrorMemoryAllocation ? KM_ENOMEM : KM_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+    } while (0)
+
+#define KM_TRY(call)                              \
+    do {                                          \
+        km_status s_ = (call);                    \
+        if (s_ != KM_OK) return s_;               \
+    } while (0)
+
+// ---- NCCL, loaded on demand ---------------------------------------------------------------
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                              ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi *nccl()
+{
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api.ok ? &api : nullptr;
+    tried = true;
+    const char *env = getenv("KM_NCCL_LIB");
+    const char *names[] = {env, "libnccl.so.2", "libnccl.so"};
+    void *h = nullptr;
+    for (const char *nm : names)
+        if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return nullptr;
+#define SYM(f, s) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, s))
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.GroupStart &&
+             api.GroupEnd && api.CommDestroy && api.GetErrorString;
+    return api.ok ? &api : nullptr;
+}
+
+struct HostStat {
+    unsigned long long local[4];   // changed, dists, clause1, refined (this rank)
+    unsigned long long global[4];  // after allreduce
+    int empty;
+    int pad;
+};
+
+int pad_dim(int d)
+{
+    for (int p : {4, 8, 16, 32, 64})
+        if (d <= p) return p;
+    return -1;
+}
+
+int next_pow2(int v)
+{
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+}  // namespace
+
+struct km_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int64_t n = 0;
+    int d = 0, DP = 0, k = 0, prune = KM_PRUNE_MTI, rank = 0, world = 1, num_sms = 148;
+    int64_t n_global = 0;
+    bool csmem = false;
+    // row data (ping-pong for re-bucketing)
+    float *X[2] = {nullptr, nullptr};
+    int32_t *a[2] = {nullptr, nullptr};
+    float *u[2] = {nullptr, nullptr};
+    int32_t *perm[2] = {nullptr, nullptr};
+    int cur = 0;
+    // sort scratch
+    uint32_t *keys = nullptr, *hist = nullptr, *totals = nullptr, *base = nullptr;
+    int Q = 1, NB = 0, ntiles = 0, tile_rows = 32768;
+    // centroid state
+    double *C = nullptr, *Cprev = nullptr;
+    float *Cneg = nullptr, *f = nullptr, *s = nullptr;
+    uint64_t *NL = nullptr;
+    // per-iteration scratch (zeroed by one memset): acc | counters | empty, eps_bits, work[2]
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    double *acc = nullptr;
+    unsigned long long *counters = nullptr, *counters_g = nullptr;
+    int *empty = nullptr, *work = nullptr;
+    unsigned *eps_bits = nullptr;
+    double *sse_buf = nullptr;
+    int32_t *a_out = nullptr;
+    HostStat *hstat = nullptr;
+    int grid_assign[4] = {0, 0, 0, 0};
+    float g_up = 1.f, g_dn = 1.f;
+    int t = 0;
+    int64_t changed_since_sort = 0;
+    int resort_policy = KM_RESORT_AUTO;
+    float resort_fraction = 0.10f;
+    std::vector<km_iter_stats> stats;
+    cudaEvent_t ev[7] = {};
+    ncclComm_t comm = nullptr;
+    int64_t launches = 0;
+};
+
+namespace {
+
+km_status prep(km_ctx *c)
+{
+    km::PrepParams p;
+    p.C = c->C;
+    p.Cprev = c->Cprev;
+    p.k = c->k;
+    p.d = c->d;
+    p.DP = c->DP;
+    p.sortN = std::max(2, next_pow2(c->k));
+    p.Cneg = c->Cneg;
+    p.f = c->f;
+    p.s = c->s;
+    p.NL = c->NL;
+    p.eps_bits = c->eps_bits;
+    KM_CUDA(km::launch_prep(p, c->st));
+    c->launches += 1;
+    return KM_OK;
+}
+
+km::AssignParams assign_params(km_ctx *c, int work_slot)
+{
+    km::AssignParams p;
+    p.X = c->X[c->cur];
+    p.a = c->a[c->cur];
+    p.u = c->u[c->cur];
+    p.n = c->n;
+    p.d = c->d;
+    p.k = c->k;
+    p.Cneg = c->Cneg;
+    p.C64 = c->C;
+    p.NL = c->NL;
+    p.f = c->f;
+    p.s = c->s;
+    p.eps = reinterpret_cast<const float *>(c->eps_bits);
+    p.g_up = c->g_up;
+    p.g_dn = c->g_dn;
+    p.count_changed = c->t > 1;
+    p.acc = c->acc;
+    p.counters = c->counters;
+    p.work = c->work + work_slot;
+    return p;
+}
+
+km_status launch_assign(km_ctx *c, int mode, int work_slot)
+{
+    km::AssignParams p = assign_params(c, work_slot);
+    KM_CUDA(km::launch_assign(mode, c->DP, c->csmem, p, c->grid_assign[mode], c->st));
+    c->launches += 1;
+    return KM_OK;
+}
+
+km_status resort(km_ctx *c)
+{
+    km::SortParams p;
+    const int o = c->cur, nw = 1 - c->cur;
+    p.X = c->X[o]; p.a = c->a[o]; p.u = c->u[o]; p.perm = c->perm[o];
+    p.X2 = c->X[nw]; p.a2 = c->a[nw]; p.u2 = c->u[nw]; p.perm2 = c->perm[nw];
+    p.keys = c->keys; p.hist = c->hist; p.totals = c->totals; p.base = c->base;
+    p.NL = c->NL; p.s = c->s;
+    p.n = c->n; p.k = c->k; p.DP = c->DP;
+    p.Q = c->prune == KM_PRUNE_MTI ? c->Q : 1;
+    p.NB = c->k * p.Q;
+    p.ntiles = c->ntiles;
+    p.tile_rows = c->tile_rows;
+    int l = 0;
+    KM_CUDA(km::launch_sort(p, c->st, &l));
+    c->launches += l;
+    c->cur = nw;
+    c->changed_since_sort = 0;
+    return KM_OK;
+}
+
+km_status allreduce(km_ctx *c)
+{
+    if (c->world <= 1) {
+        KM_CUDA(cudaMemcpyAsync(c->counters_g, c->counters, 4 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToDevice, c->st));
+        return KM_OK;
+    }
+    NcclApi *N = nccl();
+    if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable");
+    ncclResult_t r;
+    N->GroupStart();
+    r = N->AllReduce(c->acc, c->acc, (size_t)c->k * (c->DP + 1), ncclFloat64, ncclSum, c->comm, c->st);
+    if (r == ncclSuccess)
+        r = N->AllReduce(c->counters, c->counters_g, 4, ncclUint64, ncclSum, c->comm, c->st);
+    ncclResult_t r2 = N->GroupEnd();
+    if (r != ncclSuccess) return fail(KM_ENCCL, "ncclAllReduce: %s", N->GetErrorString(r));
+    if (r2 != ncclSuccess) return fail(KM_ENCCL, "ncclGroupEnd: %s", N->GetErrorString(r2));
+    return KM_OK;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b)
+{
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) ms = 0.f;
+    return ms;
+}
+
+km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
+{
+    KM_CUDA(cudaSetDevice(c->device));
+    cudaEvent_t *ev = c->ev;
+    const bool first = c->t == 0;
+    c->t += 1;
+    km_iter_stats rec;
+    memset(&rec, 0, sizeof rec);
+    KM_CUDA(cudaEventRecord(ev[0], c->st));
+    // re-bucket before the pass when the layout has drifted (u and NL of the previous pass)
+    bool sorted_now = false;
+    if (!first) {
+        bool need = false;
+        if (c->resort_policy == KM_RESORT_ALWAYS) need = true;
+        else if (c->resort_policy == KM_RESORT_AUTO)
+            need = (double)c->changed_since_sort > (double)c->resort_fraction * (double)c->n;
+        if (need) {
+            KM_TRY(resort(c));
+            sorted_now = true;
+        }
+    }
+    KM_CUDA(cudaEventRecord(ev[1], c->st));
+    KM_CUDA(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, c->st));
+    KM_TRY(prep(c));
+    KM_CUDA(cudaEventRecord(ev[2], c->st));
+    if (first) {
+        KM_TRY(launch_assign(c, km::MODE_DENSE, 0));
+        KM_CUDA(cudaEventRecord(ev[3], c->st));
+        if (c->resort_policy != KM_RESORT_NEVER) {
+            KM_TRY(resort(c));
+            sorted_now = true;
+        }
+        KM_TRY(launch_assign(c, km::MODE_REDUCE_ONLY, 1));
+    } else {
+        KM_TRY(launch_assign(c, c->prune == KM_PRUNE_MTI ? km::MODE_MTI_REDUCE : km::MODE_DENSE_REDUCE, 0));
+        KM_CUDA(cudaEventRecord(ev[3], c->st));
+    }
+    KM_CUDA(cudaEventRecord(ev[4], c->st));
+    KM_TRY(allreduce(c));
+    KM_CUDA(cudaEventRecord(ev[5], c->st));
+    KM_CUDA(km::launch_update(c->acc, c->C, c->Cprev, c->k, c->d, c->DP, c->empty, c->st));
+    c->launches += 1;
+    KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 4 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 4 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(cudaMemcpyAsync(&c->hstat->empty, c->empty, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(cudaEventRecord(ev[6], c->st));
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    HostStat *h = c->hstat;
+    if (first) {
+        rec.changed = c->n_global;
+        rec.dists = c->n_global * (int64_t)c->k;
+        c->changed_since_sort = 0;
+    } else {
+        rec.changed = (int64_t)h->global[0];
+        rec.dists = (int64_t)h->global[1];
+        c->changed_since_sort += (int64_t)h->local[0];
+    }
+    rec.clause1 = (int64_t)h->global[2];
+    rec.refined = (int64_t)h->global[3];
+    rec.empty = h->empty;
+    rec.resorted = sorted_now;
+    rec.ms_assign = elapsed(ev[2], ev[3]);
+    rec.ms_sort = first ? elapsed(ev[3], ev[4]) : elapsed(ev[0], ev[1]);
+    rec.ms_comm = c->world > 1 ? elapsed(ev[4], ev[5]) : 0.f;
+    rec.ms_iter = elapsed(ev[0], ev[6]);
+    c->stats.push_back(rec);
+    if (changed_out) *changed_out = rec.changed;
+    if (dists_out) *dists_out = rec.dists;
+    return KM_OK;
+}
+
+void free_all(km_ctx *c)
+{
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(c->X[i]); cudaFree(c->a[i]); cudaFree(c->u[i]); cudaFree(c->perm[i]);
+    }
+    cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base);
+    cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
+    cudaFree(c->NL); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
+    cudaFree(c->counters_g);
+    if (c->hstat) cudaFreeHost(c->hstat);
+    for (auto &e : c->ev) if (e) cudaEventDestroy(e);
+    if (c->comm) { NcclApi *N = nccl(); if (N) N->CommDestroy(c->comm); }
+    if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+}
+
+template <typename T>
+km_status dalloc(T **p, size_t count)
+{
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess)
+        return fail(KM_ENOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+    return KM_OK;
+}
+
+km_status create(int64_t n, int32_t d, int32_t k, const float *points, const double *C0,
+                 const km_options *o, km_ctx *c)
+{
+    c->device = o->device;
+    KM_CUDA(cudaSetDevice(c->device));
+    c->n = n; c->d = d; c->k = k; c->DP = pad_dim(d);
+    c->prune = o->prune; c->rank = o->rank; c->world = o->world;
+    c->n_global = o->n_global > 0 ? o->n_global : n * (int64_t)o->world;
+    c->resort_policy = o->resort_policy;
+    c->resort_fraction = o->resort_fraction > 0.f ? o->resort_fraction : 0.10f;
+    KM_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    if (o->stream) {
+        c->st = static_cast<cudaStream_t>(o->stream);
+    } else {
+        KM_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    for (auto &e : c->ev) KM_CUDA(cudaEventCreate(&e));
+    const int DP = c->DP;
+    c->csmem = (size_t)k * DP * sizeof(float) <= 48 * 1024;
+    // exact-mode gamma = (DP + 3) 2^-24 on the distance scale
+    const double gamma = (DP + 3) * std::ldexp(1.0, -24);
+    c->g_up = std::nextafter((float)(1.0 + gamma), 2.0f);
+    c->g_dn = std::nextafter((float)(1.0 - gamma), 0.0f);
+    // buffers
+    for (int i = 0; i < 2; ++i) {
+        KM_TRY(dalloc(&c->X[i], (size_t)n * DP));
+        KM_TRY(dalloc(&c->a[i], (size_t)n));
+        KM_TRY(dalloc(&c->u[i], (size_t)n));
+        KM_TRY(dalloc(&c->perm[i], (size_t)n));
+    }
+    c->Q = std::max(1, std::min(32, 4096 / k));
+    const int NBmax = k * c->Q;
+    c->ntiles = (int)((n + c->tile_rows - 1) / c->tile_rows);
+    KM_TRY(dalloc(&c->keys, (size_t)n));
+    KM_TRY(dalloc(&c->hist, (size_t)NBmax * c->ntiles));
+    KM_TRY(dalloc(&c->totals, (size_t)NBmax));
+    KM_TRY(dalloc(&c->base, (size_t)NBmax));
+    KM_TRY(dalloc(&c->C, (size_t)k * d));
+    KM_TRY(dalloc(&c->Cprev, (size_t)k * d));
+    KM_TRY(dalloc(&c->Cneg, (size_t)k * DP));
+    KM_TRY(dalloc(&c->f, (size_t)k));
+    KM_TRY(dalloc(&c->s, (size_t)k));
+    KM_TRY(dalloc(&c->NL, (size_t)k * std::max(1, k - 1)));
+    const size_t acc_bytes = (size_t)k * (DP + 1) * sizeof(double);
+    c->scratch_bytes = acc_bytes + 4 * sizeof(unsigned long long) + 8 * sizeof(int);
+    KM_CUDA(cudaMalloc(&c->scratch, c->scratch_bytes));
+    c->acc = static_cast<double *>(c->scratch);
+    c->counters = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->scratch) + acc_bytes);
+    int *ints = reinterpret_cast<int *>(c->counters + 4);
+    c->empty = ints + 0;
+    c->eps_bits = reinterpret_cast<unsigned *>(ints + 1);
+    c->work = ints + 2;   // two work counters
+    KM_TRY(dalloc(&c->counters_g, 4));
+    KM_TRY(dalloc(&c->sse_buf, 1));
+    KM_CUDA(cudaMallocHost(&c->hstat, sizeof(HostStat)));
+    // points -> private padded copy
+    float *X0 = c->X[0];
+    if (DP != d) KM_CUDA(cudaMemsetAsync(X0, 0, (size_t)n * DP * sizeof(float), c->st));
+    KM_CUDA(cudaMemcpy2DAsync(X0, DP * sizeof(float), points, d * sizeof(float), d * sizeof(float),
+                              (size_t)n, o->points_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                              c->st));
+    KM_CUDA(km::launch_iota(c->perm[0], n, c->st));
+    c->launches += 1;
+    KM_CUDA(cudaMemcpyAsync(c->C, C0, (size_t)k * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    KM_CUDA(cudaMemcpyAsync(c->Cprev, C0, (size_t)k * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    if (o->check_finite) {
+        for (int64_t i = 0; i < (int64_t)k * d; ++i)
+            if (!std::isfinite(C0[i])) return fail(KM_ENONFINITE, "init_centroids[%lld] is not finite", (long long)i);
+        KM_CUDA(cudaMemsetAsync(c->work, 0, sizeof(int), c->st));
+        KM_CUDA(km::launch_check_finite(X0, (int64_t)n * DP, c->work, c->st));
+        c->launches += 1;
+        int flag = 0;
+        KM_CUDA(cudaMemcpyAsync(&flag, c->work, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+        KM_CUDA(cudaStreamSynchronize(c->st));
+        if (flag) return fail(KM_ENONFINITE, "points contain NaN or Inf");
+    }
+    for (int m = 0; m < 4; ++m) c->grid_assign[m] = km::assign_grid(m, DP, c->csmem, k, c->num_sms);
+    if (c->world > 1) {
+        NcclApi *N = nccl();
+        if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable (world=%d)", c->world);
+        ncclUniqueId id;
+        memcpy(id.internal, o->nccl_unique_id, sizeof(id.internal));
+        ncclResult_t r = N->CommInitRank(&c->comm, c->world, id, c->rank);
+        if (r != ncclSuccess) return fail(KM_ENCCL, "ncclCommInitRank: %s", N->GetErrorString(r));
+    }
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    return KM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void kmeans_default_options(km_options *o)
+{
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->prune = KM_PRUNE_MTI;
+    o->world = 1;
+    o->resort_policy = KM_RESORT_AUTO;
+    o->resort_fraction = 0.10f;
+}
+
+km_status kmeans_nccl_unique_id(uint8_t out[128])
+{
+    if (!out) return fail(KM_EARG, "out is NULL");
+    NcclApi *N = nccl();
+    if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    ncclResult_t r = N->GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(KM_ENCCL, "ncclGetUniqueId: %s", N->GetErrorString(r));
+    memcpy(out, id.internal, 128);
+    return KM_OK;
+}
+
+km_status kmeans_create(int64_t n_local, int32_t d, int32_t k, const float *points,
+                        const double *init_centroids, const km_options *opt, km_ctx **out)
+{
+    g_err.clear();
+    if (!out) return fail(KM_EARG, "out is NULL");
+    *out = nullptr;
+    km_options o;
+    if (opt) o = *opt; else kmeans_default_options(&o);
+    if (o.world < 1) o.world = 1;
+    const int64_t ng = o.n_global > 0 ? o.n_global : n_local * (int64_t)o.world;
+    if (n_local < 1 || n_local > 0x7fffffffLL) return fail(KM_EARG, "n_local=%lld out of range", (long long)n_local);
+    if (d < 1 || d > 64) return fail(KM_EARG, "d=%d out of range [1, 64]", d);
+    if (k < 1 || k > 4096 || k > ng) return fail(KM_EARG, "k=%d out of range [1, min(4096, n_global=%lld)]", k, (long long)ng);
+    if (!points || !init_centroids) return fail(KM_EARG, "points/init_centroids is NULL");
+    if (reinterpret_cast<uintptr_t>(points) % 4) return fail(KM_EARG, "points not 4-byte aligned");
+    if (o.rank < 0 || o.rank >= o.world) return fail(KM_EARG, "rank=%d world=%d", o.rank, o.world);
+    if (o.prune != KM_PRUNE_MTI && o.prune != KM_PRUNE_NONE) return fail(KM_EARG, "prune=%d", o.prune);
+    if (o.resort_policy < 0 || o.resort_policy > 2) return fail(KM_EARG, "resort_policy=%d", o.resort_policy);
+    o.n_global = ng;
+    km_ctx *c = new km_ctx();
+    km_status s = create(n_local, d, k, points, init_centroids, &o, c);
+    if (s != KM_OK) {
+        std::string keep = g_err;
+        free_all(c);
+        delete c;
+        g_err = keep;
+        return s;
+    }
+    *out = c;
+    return KM_OK;
+}
+
+km_status kmeans_iterate(km_ctx *c, int64_t *changed, int64_t *dists)
+{
+    g_err.clear();
+    if (!c) return fail(KM_EARG, "ctx is NULL");
+    return iterate(c, changed, dists);
+}
+
+km_status kmeans_run(km_ctx *c, int32_t max_iters, int64_t tol, int32_t *iterations, int64_t *dists_total)
+{
+    g_err.clear();
+    if (!c) return fail(KM_EARG, "ctx is NULL");
+    if (max_iters < 0) return fail(KM_EARG, "max_iters=%d", max_iters);
+    int it = 0;
+    int64_t tot = 0;
+    for (; it < max_iters;) {
+        int64_t ch = 0, ds = 0;
+        km_status s = iterate(c, &ch, &ds);
+        if (s != KM_OK) return s;
+        ++it;
+        tot += ds;
+        if (ch <= tol) break;
+    }
+    if (iterations) *iterations = it;
+    if (dists_total) *dists_total = tot;
+    return KM_OK;
+}
+
+km_status kmeans_get_assignments(km_ctx *c, int32_t *out, int32_t out_is_device)
+{
+    g_err.clear();
+    if (!c || !out) return fail(KM_EARG, "NULL argument");
+    if (c->t == 0) return fail(KM_ESTATE, "no assignment pass has run yet");
+    KM_CUDA(cudaSetDevice(c->device));
+    if (!c->a_out) KM_TRY(dalloc(&c->a_out, (size_t)c->n));
+    KM_CUDA(km::launch_unpermute(c->a[c->cur], c->perm[c->cur], c->n, c->a_out, c->st));
+    c->launches += 1;
+    KM_CUDA(cudaMemcpyAsync(out, c->a_out, (size_t)c->n * sizeof(int32_t),
+                            out_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    return KM_OK;
+}
+
+km_status kmeans_get_centroids(km_ctx *c, double *out)
+{
+    g_err.clear();
+    if (!c || !out) return fail(KM_EARG, "NULL argument");
+    KM_CUDA(cudaSetDevice(c->device));
+    KM_CUDA(cudaMemcpyAsync(out, c->C, (size_t)c->k * c->d * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    return KM_OK;
+}
+
+km_status kmeans_set_centroids(km_ctx *c, const double *cent)
+{
+    g_err.clear();
+    if (!c || !cent) return fail(KM_EARG, "NULL argument");
+    KM_CUDA(cudaSetDevice(c->device));
+    KM_CUDA(cudaMemcpyAsync(c->C, cent, (size_t)c->k * c->d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    if (c->t == 0)   // before iteration 1 there is no previous pass: drift reference = C
+        KM_CUDA(cudaMemcpyAsync(c->Cprev, cent, (size_t)c->k * c->d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    return KM_OK;
+}
+
+km_status kmeans_sse(km_ctx *c, double *out)
+{
+    g_err.clear();
+    if (!c || !out) return fail(KM_EARG, "NULL argument");
+    if (c->t == 0) return fail(KM_ESTATE, "no assignment pass has run yet");
+    KM_CUDA(cudaSetDevice(c->device));
+    KM_CUDA(cudaMemsetAsync(c->sse_buf, 0, sizeof(double), c->st));
+    KM_CUDA(km::launch_sse(c->X[c->cur], c->a[c->cur], c->C, c->n, c->d, c->DP, c->sse_buf, c->st));
+    c->launches += 1;
+    if (c->world > 1) {
+        NcclApi *N = nccl();
+        if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable");
+        ncclResult_t r = N->AllReduce(c->sse_buf, c->sse_buf, 1, ncclFloat64, ncclSum, c->comm, c->st);
+        if (r != ncclSuccess) return fail(KM_ENCCL, "ncclAllReduce: %s", N->GetErrorString(r));
+    }
+    KM_CUDA(cudaMemcpyAsync(out, c->sse_buf, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    return KM_OK;
+}
+
+km_status kmeans_get_stats(km_ctx *c, km_iter_stats *out, int32_t cap, int32_t *count)
+{
+    g_err.clear();
+    if (!c) return fail(KM_EARG, "ctx is NULL");
+    const int32_t m = (int32_t)c->stats.size();
+    if (count) *count = m;
+    if (out && cap > 0) memcpy(out, c->stats.data(), sizeof(km_iter_stats) * (size_t)std::min(cap, m));
+    return KM_OK;
+}
+
+int64_t kmeans_launch_count(const km_ctx *c) { return c ? c->launches : 0; }
+
+void kmeans_destroy(km_ctx *c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->st) cudaStreamSynchronize(c->st);
+    free_all(c);
+    delete c;
+}
+
+const char *kmeans_last_error(void) { return g_err.c_str(); }
+
+const char *kmeans_version(void) { return "kmeans_b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

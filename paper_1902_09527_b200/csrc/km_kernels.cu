@@ -1,0 +1,748 @@
+// km_kernels.cu — sm_100a kernels for MTI-pruned Lloyd's k-means.
+//
+//   k_prep        S1: centroid geometry + drift from the fp64 master centroids
+//                 (PAPER.md:990-991 drift f; PAPER.md:1036-1040 clause-1 radius; reading A1/A2)
+//   k_assign      S0/S2(+S3): dense or MTI assignment with exact-mode fp64 refinement, fused
+//                 with the per-cluster fp64 reduction
+//   k_update      S4: centroid update, empty cluster keeps its centroid (reading A10)
+//   k_sort_*      re-bucketing of rows by (cluster, survivor-prefix class): B200-specific
+//                 layout step so warps walk one cluster's neighbour list with broadcast reads
+//   k_sse         S5: SSE (Eq. 1 as SSE; reading A15)
+#include "km_kernels.cuh"
+
+#include <math.h>
+
+namespace km {
+
+// ---------------------------------------------------------------------------------------
+// packed fp32x2 arithmetic (sm_100a FADD2/FFMA2)
+__device__ __forceinline__ float2 add2(float2 a, float2 b)
+{
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rr;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rr, ra, rb;\n\tmov.b64 {%0, %1}, rr;\n\t}"
+        : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c)
+{
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc, rr;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rr, ra, rb, rc;\n\tmov.b64 {%0, %1}, rr;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+
+// Squared distance ||x - c||^2 in fp32, direct-difference form: t = x + (-c) (IEEE x - c),
+// squares accumulated with fma in four interleaved partial sums.  Relative error of the
+// result <= (DP/4 + 4) * 2^-24 (+O(2^-48)); DESIGN.md "Exact mode" bounds sqrt of it by gamma.
+template <int DP, bool SMEM>
+__device__ __forceinline__ float dist2(const float (&x)[DP], const float *cneg)
+{
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < DP; j += 4) {
+        float4 c = SMEM ? *reinterpret_cast<const float4 *>(cneg + j)
+                        : __ldg(reinterpret_cast<const float4 *>(cneg + j));
+        float2 t0 = add2(make_float2(x[j], x[j + 1]), make_float2(c.x, c.y));
+        float2 t1 = add2(make_float2(x[j + 2], x[j + 3]), make_float2(c.z, c.w));
+        acc0 = fma2(t0, t0, acc0);
+        acc1 = fma2(t1, t1, acc1);
+    }
+    float2 s = add2(acc0, acc1);
+    return s.x + s.y;
+}
+
+// Rigorous distance interval of an fp32 squared distance q (exact mode):
+// true d(x, C64[c]) in [lower, upper] (gamma folded into g_up/g_dn, eps = eps_C).
+__device__ __forceinline__ float upper_d(float q, float g_up, float eps)
+{
+    return __fadd_ru(__fmul_ru(__fsqrt_ru(q), g_up), eps);
+}
+__device__ __forceinline__ float lower_d(float q, float g_dn, float eps)
+{
+    return fmaxf(0.f, __fsub_rd(__fmul_rd(__fsqrt_rd(q), g_dn), eps));
+}
+
+__device__ __forceinline__ float key_h(uint64_t key) { return __uint_as_float((uint32_t)(key >> 32)); }
+__device__ __forceinline__ int key_c(uint64_t key) { return (int)(uint32_t)(key & 0xffffffffull); }
+
+// fp64 re-evaluation (exact mode): argmin over {A} u {c' : H[A][c'] < ut} (MTI) or over
+// all k (nl == nullptr), lowest index on ties; distances in the oracle's direct form.
+__device__ __noinline__ int refine64(const float *xrow, int d, const double *C64, int k, int A,
+                                     const uint64_t *nl, float ut, float *unew)
+{
+    double best = INFINITY;
+    int bc = 0x7fffffff;
+    auto eval = [&](int c) {
+        const double *cc = C64 + (int64_t)c * d;
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) {
+            double t = __dsub_rn((double)xrow[j], cc[j]);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+        if (s < best || (s == best && c < bc)) { best = s; bc = c; }
+    };
+    if (nl) {
+        eval(A);
+        for (int j = 0; j < k - 1; ++j) {
+            uint64_t key = nl[j];
+            if (!(key_h(key) < ut)) break;
+            eval(key_c(key));
+        }
+    } else {
+        for (int c = 0; c < k; ++c) eval(c);
+    }
+    *unew = __double2float_ru(sqrt(best) * (1.0 + 1e-12));
+    return bc;
+}
+
+// ---------------------------------------------------------------------------------------
+// warp transpose-reduction of DP fp64 values per lane: afterwards lane L holds, in v[0..W),
+// the warp sums of components tr_base(L) + i.  Uses DP-1 (+log2(32/DP)) double shuffles.
+template <int DP> struct Red {
+    static constexpr int W = DP >= 32 ? DP / 32 : 1;
+    static constexpr int LASTO = DP >= 32 ? 1 : 32 / DP;
+};
+
+template <int O, int Wc, int DP>
+__device__ __forceinline__ void tr_step(double (&v)[DP], int lane)
+{
+    if constexpr (O >= 1) {
+        if constexpr (Wc > 1) {
+            const bool up = (lane & O) != 0;
+#pragma unroll
+            for (int i = 0; i < Wc / 2; ++i) {
+                double send = up ? v[i] : v[i + Wc / 2];
+                double keep = up ? v[i + Wc / 2] : v[i];
+                v[i] = keep + __shfl_xor_sync(kFull, send, O);
+            }
+            tr_step<O / 2, Wc / 2, DP>(v, lane);
+        } else {
+            v[0] += __shfl_xor_sync(kFull, v[0], O);
+            tr_step<O / 2, 1, DP>(v, lane);
+        }
+    }
+}
+
+template <int DP>
+__device__ __forceinline__ int tr_base(int lane)
+{
+    int base = 0, w = DP;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        if (w > 1) {
+            if (lane & o) base += w / 2;
+            w >>= 1;
+        }
+    }
+    return base;
+}
+
+// Per-warp run accumulator: the fp64 sums of the current run cluster R live in registers
+// (lane-distributed components) and are flushed with fp64 RED to acc only when R changes.
+template <int DP>
+struct RunAcc {
+    int R = -1;
+    int cnt = 0;
+    double v[Red<DP>::W];
+    __device__ __forceinline__ void clear()
+    {
+#pragma unroll
+        for (int i = 0; i < Red<DP>::W; ++i) v[i] = 0.0;
+        cnt = 0;
+    }
+    __device__ __forceinline__ void flush(double *acc, int d, int lane)
+    {
+        if (R < 0) return;
+        double *row = acc + (int64_t)R * (DP + 1);
+        const bool writer = (lane & (Red<DP>::LASTO - 1)) == 0;
+        const int base = tr_base<DP>(lane);
+        if (writer) {
+#pragma unroll
+            for (int i = 0; i < Red<DP>::W; ++i)
+                if (base + i < d && v[i] != 0.0) atomicAdd(row + base + i, v[i]);
+        }
+        if (lane == 0 && cnt) atomicAdd(row + DP, (double)cnt);
+    }
+};
+
+template <int DP>
+__device__ __forceinline__ void reduce_batch(RunAcc<DP> &ra, const float (&x)[DP], int anew,
+                                             bool valid, double *acc, int d, int lane)
+{
+    unsigned mR = __ballot_sync(kFull, valid && anew == ra.R);
+    if (mR == 0) {
+        unsigned mv = __ballot_sync(kFull, valid);
+        if (mv == 0) return;
+        int M = __shfl_sync(kFull, anew, __ffs(mv) - 1);
+        ra.flush(acc, d, lane);
+        ra.clear();
+        ra.R = M;
+        mR = __ballot_sync(kFull, valid && anew == M);
+    }
+    const bool in = (mR >> lane) & 1u;
+    // first transposition step (offset 16) on fp32 values, widened to fp64 when added
+    constexpr int H = DP / 2;
+    const bool up = (lane & 16) != 0;
+    double v[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        const float lo = in ? x[i] : 0.f, hi = in ? x[i + H] : 0.f;
+        const float recv = __shfl_xor_sync(kFull, up ? lo : hi, 16);
+        v[i] = (double)(up ? hi : lo) + (double)recv;
+    }
+    tr_step<8, H, H>(v, lane);
+#pragma unroll
+    for (int i = 0; i < Red<DP>::W; ++i) ra.v[i] += v[i];
+    ra.cnt += __popc(mR);
+    if (valid && !in) {      // lane leaves the warp's run cluster: direct fp64 RED
+        double *row = acc + (int64_t)anew * (DP + 1);
+        for (int j = 0; j < d; ++j) atomicAdd(row + j, (double)x[j]);
+        atomicAdd(row + DP, 1.0);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// k_assign: one lane = one row; a warp claims kChunkRows consecutive rows at a time.
+template <int DP, int MODE, bool CSMEM>
+__global__ void __launch_bounds__(kAssignThreads)
+k_assign(AssignParams p)
+{
+    constexpr bool PRUNE = MODE == MODE_MTI_REDUCE;
+    constexpr bool DENSE = MODE == MODE_DENSE || MODE == MODE_DENSE_REDUCE;
+    constexpr bool ASSIGN = MODE != MODE_REDUCE_ONLY;
+    constexpr bool REDUCE = MODE != MODE_DENSE;
+
+    extern __shared__ __align__(16) float smem[];
+    const int k = p.k;
+    float *sC = smem;                               // k*DP (CSMEM)
+    float *sF = smem + (CSMEM ? k * DP : 0);        // k
+    float *sS = sF + k;                             // k
+    if (ASSIGN) {
+        if (CSMEM) {
+            const float4 *src = reinterpret_cast<const float4 *>(p.Cneg);
+            float4 *dst = reinterpret_cast<float4 *>(sC);
+            for (int i = threadIdx.x; i < k * DP / 4; i += blockDim.x) dst[i] = src[i];
+        }
+        if (PRUNE)
+            for (int i = threadIdx.x; i < k; i += blockDim.x) { sF[i] = p.f[i]; sS[i] = p.s[i]; }
+    }
+    __syncthreads();
+    const float *Cn = CSMEM ? sC : p.Cneg;
+    const float eps = ASSIGN ? *p.eps : 0.f;
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t n = p.n;
+
+    RunAcc<DP> ra;
+    ra.clear();
+    unsigned long long c_changed = 0, c_dists = 0, c_clause1 = 0, c_refined = 0;
+
+    for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(p.work, 1);
+        chunk = __shfl_sync(kFull, chunk, 0);
+        const int64_t row0 = (int64_t)chunk * kChunkRows;
+        if (row0 >= n) break;
+#pragma unroll 1
+        for (int b = 0; b < kChunkRows / kWarp; ++b) {
+            const int64_t row = row0 + b * kWarp + lane;
+            const bool valid = row < n;
+            if (!__any_sync(kFull, valid)) break;
+            float x[DP];
+            {
+                const float4 *xr = reinterpret_cast<const float4 *>(p.X + (valid ? row : 0) * DP);
+#pragma unroll
+                for (int j = 0; j < DP / 4; ++j) {
+                    float4 t = valid ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    x[4 * j] = t.x; x[4 * j + 1] = t.y; x[4 * j + 2] = t.z; x[4 * j + 3] = t.w;
+                }
+            }
+            const int aold = valid ? p.a[row] : 0;
+            int anew = aold;
+            if (ASSIGN) {
+                float unew = 0.f;
+                bool active = valid;
+                if (PRUNE) {
+                    const float uu = valid ? __fadd_ru(p.u[row], sF[aold]) : 0.f;  // u += f(a)
+                    const bool c1 = valid && uu <= sS[aold];                       // clause 1
+                    c_clause1 += c1;
+                    active = valid && !c1;
+                    unew = uu;
+                }
+                if (__any_sync(kFull, active)) {
+                    float bq = INFINITY, q2 = INFINITY, ut = 0.f;
+                    int bc = aold, ns = 0;
+                    if (DENSE) {
+#pragma unroll 1
+                        for (int c = 0; c < k; ++c) {
+                            const float q = dist2<DP, CSMEM>(x, Cn + c * DP);
+                            if (q < bq) { q2 = bq; bq = q; bc = c; }
+                            else if (q < q2) { q2 = q; }
+                        }
+                        ns = k;
+                    } else {
+                        // group the warp by assigned cluster; each group walks its cluster's
+                        // neighbour list (ascending H) with broadcast centroid reads
+                        unsigned rem = __ballot_sync(kFull, active);
+                        while (rem) {
+                            const int A = __shfl_sync(kFull, aold, __ffs(rem) - 1);
+                            const bool mine = active && aold == A;
+                            rem &= ~__ballot_sync(kFull, mine);
+                            if (mine) {                         // tighten: U(u) = d(x, C[a])
+                                bq = dist2<DP, CSMEM>(x, Cn + A * DP);
+                                bc = A;
+                                ut = upper_d(bq, p.g_up, eps);
+                                ns = 1;
+                            }
+                            const uint64_t *nl = p.NL + (int64_t)A * (k - 1);
+#pragma unroll 1
+                            for (int j = 0; j < k - 1; ++j) {
+                                const uint64_t key = __ldg(nl + j);
+                                const bool go = mine && key_h(key) < ut;   // clauses 2/3
+                                if (!__any_sync(kFull, go)) break;
+                                if (go) {
+                                    const int c = key_c(key);
+                                    const float q = dist2<DP, CSMEM>(x, Cn + c * DP);
+                                    ++ns;
+                                    if (q < bq || (q == bq && c < bc)) { q2 = bq; bq = q; bc = c; }
+                                    else if (q < q2) { q2 = q; }
+                                }
+                            }
+                        }
+                    }
+                    if (active) {
+                        const float ub = upper_d(bq, p.g_up, eps);
+                        const bool amb = q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub;
+                        if (amb) {
+                            anew = refine64(p.X + row * DP, p.d, p.C64, k, aold,
+                                            DENSE ? nullptr : p.NL + (int64_t)aold * (k - 1),
+                                            ut, &unew);
+                            ++c_refined;
+                        } else {
+                            anew = bc;
+                            unew = ub;
+                        }
+                        c_dists += (unsigned long long)ns;
+                    }
+                }
+                if (valid) {
+                    p.a[row] = anew;
+                    p.u[row] = unew;
+                    if (p.count_changed) c_changed += (anew != aold);
+                }
+            }
+            if (REDUCE) reduce_batch<DP>(ra, x, anew, valid, p.acc, p.d, lane);
+        }
+    }
+    if (REDUCE) ra.flush(p.acc, p.d, lane);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        c_changed += __shfl_xor_sync(kFull, c_changed, o);
+        c_dists += __shfl_xor_sync(kFull, c_dists, o);
+        c_clause1 += __shfl_xor_sync(kFull, c_clause1, o);
+        c_refined += __shfl_xor_sync(kFull, c_refined, o);
+    }
+    if (lane == 0 && ASSIGN) {
+        if (c_changed) atomicAdd(p.counters + 0, c_changed);
+        if (c_dists) atomicAdd(p.counters + 1, c_dists);
+        if (c_clause1) atomicAdd(p.counters + 2, c_clause1);
+        if (c_refined) atomicAdd(p.counters + 3, c_refined);
+    }
+}
+
+size_t assign_smem(int DP, bool csmem, int k)
+{
+    return (size_t)((csmem ? k * DP : 0) + 2 * k) * sizeof(float);
+}
+
+template <int DP, int MODE, bool CSMEM>
+static cudaError_t launch_assign_t(const AssignParams &p, int grid, cudaStream_t st)
+{
+    const size_t sm = assign_smem(DP, CSMEM, p.k);
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_assign<DP, MODE, CSMEM>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+    }
+    k_assign<DP, MODE, CSMEM><<<grid, kAssignThreads, sm, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int DP, int MODE, bool CSMEM>
+static int grid_t(int k, int num_sms)
+{
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_assign<DP, MODE, CSMEM>, kAssignThreads,
+                                                  assign_smem(DP, CSMEM, k));
+    if (per_sm < 1) per_sm = 1;
+    return per_sm * num_sms;
+}
+
+#define KM_DISPATCH_DP(DPV, FN, ...)                                   \
+    switch (DPV) {                                                     \
+    case 4: return FN<4, __VA_ARGS__>;                                 \
+    case 8: return FN<8, __VA_ARGS__>;                                 \
+    case 16: return FN<16, __VA_ARGS__>;                               \
+    case 32: return FN<32, __VA_ARGS__>;                               \
+    case 64: return FN<64, __VA_ARGS__>;                               \
+    default: return nullptr;                                           \
+    }
+
+typedef cudaError_t (*assign_fn)(const AssignParams &, int, cudaStream_t);
+typedef int (*grid_fn)(int, int);
+
+template <int MODE, bool CSMEM>
+static assign_fn pick_assign(int DP) { KM_DISPATCH_DP(DP, launch_assign_t, MODE, CSMEM) }
+template <int MODE, bool CSMEM>
+static grid_fn pick_grid(int DP) { KM_DISPATCH_DP(DP, grid_t, MODE, CSMEM) }
+
+static assign_fn assign_table(int mode, int DP, bool cs)
+{
+    switch (mode * 2 + (cs ? 1 : 0)) {
+    case 0: return pick_assign<MODE_DENSE, false>(DP);
+    case 1: return pick_assign<MODE_DENSE, true>(DP);
+    case 2: return pick_assign<MODE_DENSE_REDUCE, false>(DP);
+    case 3: return pick_assign<MODE_DENSE_REDUCE, true>(DP);
+    case 4: return pick_assign<MODE_MTI_REDUCE, false>(DP);
+    case 5: return pick_assign<MODE_MTI_REDUCE, true>(DP);
+    case 6: return pick_assign<MODE_REDUCE_ONLY, false>(DP);
+    case 7: return pick_assign<MODE_REDUCE_ONLY, true>(DP);
+    }
+    return nullptr;
+}
+
+static grid_fn grid_table(int mode, int DP, bool cs)
+{
+    switch (mode * 2 + (cs ? 1 : 0)) {
+    case 0: return pick_grid<MODE_DENSE, false>(DP);
+    case 1: return pick_grid<MODE_DENSE, true>(DP);
+    case 2: return pick_grid<MODE_DENSE_REDUCE, false>(DP);
+    case 3: return pick_grid<MODE_DENSE_REDUCE, true>(DP);
+    case 4: return pick_grid<MODE_MTI_REDUCE, false>(DP);
+    case 5: return pick_grid<MODE_MTI_REDUCE, true>(DP);
+    case 6: return pick_grid<MODE_REDUCE_ONLY, false>(DP);
+    case 7: return pick_grid<MODE_REDUCE_ONLY, true>(DP);
+    }
+    return nullptr;
+}
+
+cudaError_t launch_assign(int mode, int DP, bool csmem, const AssignParams &p, int grid,
+                          cudaStream_t st)
+{
+    assign_fn fn = assign_table(mode, DP, csmem);
+    if (!fn) return cudaErrorInvalidValue;
+    return fn(p, grid, st);
+}
+
+int assign_grid(int mode, int DP, bool csmem, int k, int num_sms)
+{
+    grid_fn fn = grid_table(mode, DP, csmem);
+    return fn ? fn(k, num_sms) : num_sms;
+}
+
+// ---------------------------------------------------------------------------------------
+// S1: per centroid c (one CTA): H[c][.] = 1/2 ||C[c] - C[.]|| rounded down to fp32, sorted
+// ascending with ties by index -> NL[c]; s[c] = NL[c][0].h (k = 1: +inf); f[c] = drift
+// rounded up; Cneg[c] = -fp32(C[c]); eps_C = max_c ||C[c] - fp32(C[c])|| rounded up.
+// The fp64 values carry relative error <= (d+2) 2^-53 < 1e-14, absorbed by the 1 -/+ 1e-14
+// factors before directed rounding to fp32.
+__global__ void k_prep(PrepParams p)
+{
+    extern __shared__ uint64_t keys[];
+    const int c = blockIdx.x, k = p.k, d = p.d, N = p.sortN;
+    const double *Cc = p.C + (int64_t)c * d;
+    for (int c2 = threadIdx.x; c2 < N; c2 += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (c2 < k && c2 != c) {
+            const double *C2 = p.C + (int64_t)c2 * d;
+            double s = 0.0;
+            for (int j = 0; j < d; ++j) {
+                double t = Cc[j] - C2[j];
+                s = fma(t, t, s);
+            }
+            float h = __double2float_rd(0.5 * sqrt(s) * (1.0 - 1e-14));
+            key = ((uint64_t)__float_as_uint(h) << 32) | (uint32_t)c2;
+        }
+        keys[c2] = key;
+    }
+    for (int j = threadIdx.x; j < p.DP; j += blockDim.x)
+        p.Cneg[(int64_t)c * p.DP + j] = j < d ? -(float)Cc[j] : 0.f;
+    if (threadIdx.x == 0) {
+        double se = 0.0, sf = 0.0;
+        const double *Cp = p.Cprev + (int64_t)c * d;
+        for (int j = 0; j < d; ++j) {
+            double e = Cc[j] - (double)(float)Cc[j];
+            se = fma(e, e, se);
+            double t = Cc[j] - Cp[j];
+            sf = fma(t, t, sf);
+        }
+        float eps = __double2float_ru(sqrt(se) * (1.0 + 1e-14));
+        atomicMax(p.eps_bits, __float_as_uint(eps));
+        p.f[c] = __double2float_ru(sqrt(sf) * (1.0 + 1e-14));
+    }
+    // bitonic sort (ascending) of N = 2^m keys
+    for (int size = 2; size <= N; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+                int lo = (i / stride) * 2 * stride + (i % stride);
+                int hi = lo + stride;
+                bool asc = (lo & size) == 0;
+                uint64_t A = keys[lo], B = keys[hi];
+                if ((A > B) == asc) { keys[lo] = B; keys[hi] = A; }
+            }
+        }
+    }
+    __syncthreads();
+    uint64_t *nl = p.NL + (int64_t)c * (k - 1);
+    for (int j = threadIdx.x; j < k - 1; j += blockDim.x) nl[j] = keys[j];
+    if (threadIdx.x == 0) p.s[c] = k > 1 ? __uint_as_float((uint32_t)(keys[0] >> 32)) : INFINITY;
+}
+
+cudaError_t launch_prep(const PrepParams &p, cudaStream_t st)
+{
+    size_t sm = (size_t)p.sortN * sizeof(uint64_t);
+    k_prep<<<p.k, 256, sm, st>>>(p);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// S4: C_new[c] = sums[c] / count[c] (IEEE fp64 division), or C_old[c] when empty (A10).
+__global__ void k_update(const double *acc, double *C, double *Cprev, int k, int d, int DP, int *empty)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)k * d) return;
+    int c = (int)(i / d), j = (int)(i % d);
+    double cnt = acc[(int64_t)c * (DP + 1) + DP];
+    double old = C[i];
+    Cprev[i] = old;
+    C[i] = cnt > 0.0 ? acc[(int64_t)c * (DP + 1) + j] / cnt : old;
+    if (j == 0 && !(cnt > 0.0)) atomicAdd(empty, 1);
+}
+
+cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, int d, int DP,
+                          int *empty, cudaStream_t st)
+{
+    int64_t tot = (int64_t)k * d;
+    k_update<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(acc, C, Cprev, k, d, DP, empty);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Re-bucketing (counting sort by bucket = a * Q + prefix class).  The prefix length
+// p = #{c' : H[a][c'] < u} is the number of candidates the point would evaluate; rows of a
+// bucket therefore have similar walk lengths, which keeps warp lanes busy.
+__device__ __forceinline__ uint32_t bucket_of(int a, float u, const uint64_t *NL, int k, int Q)
+{
+    if (Q == 1) return (uint32_t)a;
+    const uint64_t *nl = NL + (int64_t)a * (k - 1);
+    int lo = 0, hi = k - 1;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (key_h(__ldg(nl + mid)) < u) lo = mid + 1; else hi = mid;
+    }
+    int q = 0;
+    if (lo > 0) {
+        int64_t t = 1 + (int64_t)(lo - 1) * (Q - 1) / (k > 1 ? k - 1 : 1);
+        q = (int)(t < Q - 1 ? t : Q - 1);
+    }
+    return (uint32_t)a * Q + q;
+}
+
+__global__ void k_sort_keys(SortParams p)
+{
+    extern __shared__ uint32_t sh[];
+    for (int b = threadIdx.x; b < p.NB; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.x * p.tile_rows;
+    int64_t r1 = r0 + p.tile_rows;
+    if (r1 > p.n) r1 = p.n;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        uint32_t b = bucket_of(p.a[r], p.u[r], p.NL, p.k, p.Q);
+        p.keys[r] = b;
+        atomicAdd(&sh[b], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < p.NB; b += blockDim.x)
+        p.hist[(int64_t)b * p.ntiles + blockIdx.x] = sh[b];
+}
+
+// exclusive block scan helper (blockDim.x == 1024); returns exclusive prefix, *total = sum
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *total)
+{
+    __shared__ uint32_t wsum[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(kFull, s, o);
+            if (lane >= o) s += y;
+        }
+        wsum[lane] = s;
+    }
+    __syncthreads();
+    uint32_t incl = x + (w > 0 ? wsum[w - 1] : 0);
+    *total = wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return incl - v;
+}
+
+__global__ void k_scan_tiles(SortParams p)      // one CTA per bucket
+{
+    uint32_t *h = p.hist + (int64_t)blockIdx.x * p.ntiles;
+    uint32_t carry = 0;
+    for (int base = 0; base < p.ntiles; base += blockDim.x) {
+        int i = base + threadIdx.x;
+        uint32_t v = i < p.ntiles ? h[i] : 0, tot;
+        uint32_t ex = block_excl_scan(v, &tot);
+        if (i < p.ntiles) h[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) p.totals[blockIdx.x] = carry;
+}
+
+__global__ void k_scan_buckets(SortParams p)    // one CTA
+{
+    uint32_t carry = 0;
+    for (int base = 0; base < p.NB; base += blockDim.x) {
+        int i = base + threadIdx.x;
+        uint32_t v = i < p.NB ? p.totals[i] : 0, tot;
+        uint32_t ex = block_excl_scan(v, &tot);
+        if (i < p.NB) p.base[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+template <int DP>
+__global__ void k_scatter(SortParams p)
+{
+    extern __shared__ uint32_t cur[];
+    for (int b = threadIdx.x; b < p.NB; b += blockDim.x)
+        cur[b] = p.base[b] + p.hist[(int64_t)b * p.ntiles + blockIdx.x];
+    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.x * p.tile_rows;
+    int64_t r1 = r0 + p.tile_rows;
+    if (r1 > p.n) r1 = p.n;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        const uint32_t b = p.keys[r];
+        const int64_t dst = atomicAdd(&cur[b], 1u);
+        const float4 *src = reinterpret_cast<const float4 *>(p.X + r * DP);
+        float4 *dx = reinterpret_cast<float4 *>(p.X2 + dst * DP);
+#pragma unroll
+        for (int j = 0; j < DP / 4; ++j) dx[j] = __ldg(src + j);
+        p.a2[dst] = p.a[r];
+        p.u2[dst] = p.u[r];
+        p.perm2[dst] = p.perm[r];
+    }
+}
+
+cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches)
+{
+    const size_t sh = (size_t)p.NB * sizeof(uint32_t);   // NB <= 4096 -> <= 16 KB
+    k_sort_keys<<<p.ntiles, 512, sh, st>>>(p);
+    k_scan_tiles<<<p.NB, 1024, 0, st>>>(p);
+    k_scan_buckets<<<1, 1024, 0, st>>>(p);
+    switch (p.DP) {
+    case 4: k_scatter<4><<<p.ntiles, 512, sh, st>>>(p); break;
+    case 8: k_scatter<8><<<p.ntiles, 512, sh, st>>>(p); break;
+    case 16: k_scatter<16><<<p.ntiles, 512, sh, st>>>(p); break;
+    case 32: k_scatter<32><<<p.ntiles, 512, sh, st>>>(p); break;
+    case 64: k_scatter<64><<<p.ntiles, 512, sh, st>>>(p); break;
+    default: return cudaErrorInvalidValue;
+    }
+    if (launches) *launches += 4;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// S5: SSE in fp64 (x promoted, fp64 master centroids), block partials + one fp64 RED each.
+__global__ void k_sse(const float *X, const int32_t *a, const double *C, int64_t n, int d, int DP,
+                      double *out)
+{
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const float *x = X + r * DP;
+        const double *c = C + (int64_t)a[r] * d;
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) {
+            double t = __dsub_rn((double)x[j], c[j]);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+        acc += s;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (threadIdx.x == 0) atomicAdd(out, v);
+    }
+}
+
+cudaError_t launch_sse(const float *X, const int32_t *a, const double *C, int64_t n, int d,
+                       int DP, double *out, cudaStream_t st)
+{
+    k_sse<<<148 * 8, 256, 0, st>>>(X, a, C, n, d, DP, out);
+    return cudaGetLastError();
+}
+
+__global__ void k_unpermute(const int32_t *a, const int32_t *perm, int64_t n, int32_t *out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[perm[i]] = a[i];
+}
+
+cudaError_t launch_unpermute(const int32_t *a, const int32_t *perm, int64_t n, int32_t *out,
+                             cudaStream_t st)
+{
+    k_unpermute<<<148 * 8, 256, 0, st>>>(a, perm, n, out);
+    return cudaGetLastError();
+}
+
+__global__ void k_iota(int32_t *perm, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        perm[i] = (int32_t)i;
+}
+
+cudaError_t launch_iota(int32_t *perm, int64_t n, cudaStream_t st)
+{
+    k_iota<<<148 * 8, 256, 0, st>>>(perm, n);
+    return cudaGetLastError();
+}
+
+__global__ void k_check_finite(const float *X, int64_t count, int *flag)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(X[i])) { *flag = 1; return; }
+}
+
+cudaError_t launch_check_finite(const float *X, int64_t count, int *flag, cudaStream_t st)
+{
+    k_check_finite<<<148 * 8, 256, 0, st>>>(X, count, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace km

@@ -1,0 +1,89 @@
+// km_kernels.cuh — device-side building blocks and kernel launch interface for the
+// MTI-pruned Lloyd's k-means hot path on sm_100a (B200).
+//
+// Layout in HBM (per rank):
+//   X      n x DP fp32 row-major, DP = d padded to {4,8,16,32,64} with zeros, rows
+//          physically bucketed by (assigned cluster, survivor-prefix class) after iteration 1
+//   a, u   int32[n], fp32[n]   assignment and MTI upper bound, same row order as X
+//   perm   int32[n]            caller row index of each stored row
+//   Cneg   k x DP fp32         -fp32(C) (negated so x + (-c) is the IEEE x - c), zero padded
+//   NL     k x (k-1) uint64    per centroid c: (H[c][c'] as fp32 bits << 32 | c'), ascending
+//   f, s   fp32[k]             drift (rounded up) and 1/2 nearest-centroid distance (rounded down)
+//   acc    k x (DP+1) fp64     per-cluster sums (DP slots, padded ones stay 0) and count
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace km {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kAssignThreads = 256;
+constexpr int kChunkRows = 256;       // rows a warp claims per work-counter fetch
+
+// assignment kernel modes
+enum AssignMode : int {
+    MODE_DENSE = 0,          // all k centroids, writes a/u, no reduction (iteration 1)
+    MODE_DENSE_REDUCE = 1,   // all k centroids + fused reduction (knori-, t >= 2)
+    MODE_MTI_REDUCE = 2,     // MTI clauses 1-3 + fused reduction (knori, t >= 2)
+    MODE_REDUCE_ONLY = 3     // reduction of the current a (after the iteration-1 sort)
+};
+
+struct AssignParams {
+    const float *X;        // n x DP
+    int32_t *a;            // n
+    float *u;              // n
+    int64_t n;
+    int32_t d, k;
+    const float *Cneg;     // k x DP
+    const double *C64;     // k x d master centroids of this pass
+    const uint64_t *NL;    // k x (k-1)
+    const float *f;        // k
+    const float *s;        // k
+    const float *eps;      // device scalar: eps_C (rounded up)
+    float g_up, g_dn;      // 1 + gamma (rounded up), 1 - gamma (rounded down)
+    int32_t count_changed; // 1: count a_new != a_old
+    double *acc;           // k x (DP+1)
+    unsigned long long *counters;  // [0] changed [1] dists [2] clause1 [3] refined
+    int *work;             // dynamic chunk counter (zeroed before launch)
+};
+
+struct PrepParams {
+    const double *C;       // k x d (centroids of the coming pass)
+    const double *Cprev;   // k x d (centroids of the previous pass)
+    int32_t k, d, DP, sortN;
+    float *Cneg;           // k x DP
+    float *f, *s;          // k
+    uint64_t *NL;          // k x (k-1)
+    unsigned *eps_bits;    // fp32 bits of eps_C (atomicMax; zeroed before launch)
+};
+
+struct SortParams {
+    const float *X; const int32_t *a; const float *u; const int32_t *perm;
+    float *X2; int32_t *a2; float *u2; int32_t *perm2;
+    uint32_t *keys;        // n bucket ids
+    uint32_t *hist;        // NB x ntiles (counts, then exclusive offsets)
+    uint32_t *totals;      // NB
+    uint32_t *base;        // NB
+    const uint64_t *NL; const float *s;
+    int64_t n;
+    int32_t k, DP, Q, NB, ntiles, tile_rows;
+};
+
+// ---- launchers (km_kernels.cu) ----------------------------------------------------------
+cudaError_t launch_prep(const PrepParams &p, cudaStream_t st);
+cudaError_t launch_assign(int mode, int DP, bool csmem, const AssignParams &p, int grid,
+                          cudaStream_t st);
+int assign_grid(int mode, int DP, bool csmem, int k, int num_sms);
+size_t assign_smem(int DP, bool csmem, int k);
+cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, int d, int DP,
+                          int *empty, cudaStream_t st);
+cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches);
+cudaError_t launch_sse(const float *X, const int32_t *a, const double *C, int64_t n, int d,
+                       int DP, double *out, cudaStream_t st);
+cudaError_t launch_unpermute(const int32_t *a, const int32_t *perm, int64_t n, int32_t *out,
+                             cudaStream_t st);
+cudaError_t launch_iota(int32_t *perm, int64_t n, cudaStream_t st);
+cudaError_t launch_check_finite(const float *X, int64_t count, int *flag, cudaStream_t st);
+
+}  // namespace km

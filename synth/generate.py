@@ -133,12 +133,30 @@ def _mixture_task(args):
     return None
 
 
-def _make_mixture(spec: ConfigSpec, n: int, seed: int, workers: int) -> np.ndarray:
+def _mixture_task_rows(args):
+    c, lo, hi, rlo, rhi = args
+    st = _SHARED["mix"]
+    means, sig, w, seed, out = st["means"], st["sig"], st["w"], st["seed"], st["out"]
+    m = hi - lo
+    lab = _rng(seed, 1, c).choice(len(w), m, p=w)
+    z = _rng(seed, 2, c).standard_normal((m, means.shape[1]))
+    a, b = max(lo, rlo), min(hi, rhi)
+    out[a - rlo:b - rlo] = (means[lab[a - lo:b - lo]] + sig[lab[a - lo:b - lo], None]
+                            * z[a - lo:b - lo]).astype(np.float32)
+    return None
+
+
+def _make_mixture(spec: ConfigSpec, n: int, seed: int, workers: int, rows=None) -> np.ndarray:
     means, sig, w = _mixture_params(spec, spec.d, seed)
-    out = _shared_array((n, spec.d), np.float32)
+    rlo, rhi = (0, n) if rows is None else rows
+    out = _shared_array((rhi - rlo, spec.d), np.float32)
     _SHARED["mix"] = dict(means=means, sig=sig, w=w, seed=seed, out=out)
     try:
-        _pool_map(_mixture_task, list(_chunks(n)), workers)
+        if rows is None:
+            _pool_map(_mixture_task, list(_chunks(n)), workers)
+        else:
+            tasks = [(c, lo, hi, rlo, rhi) for (c, lo, hi) in _chunks(n) if hi > rlo and lo < rhi]
+            _pool_map(_mixture_task_rows, tasks, workers)
     finally:
         _SHARED.pop("mix", None)
     return out
@@ -154,15 +172,17 @@ def _spectral_dot_task(args):
 def _spectral_fill_task(args):
     j, c, lo, hi, seed = args
     st = _SHARED["spec"]
-    raw = _rng(seed, 2, j, c).standard_t(3, hi - lo)
-    st["out"][lo:hi, j] = ((raw / st["norm"][j]) / (j + 1)).astype(np.float32)
+    rlo, rhi = st["rows"]
+    a, b = max(lo, rlo), min(hi, rhi)
+    raw = _rng(seed, 2, j, c).standard_t(3, hi - lo)[a - lo:b - lo]
+    st["out"][a - rlo:b - rlo, j] = ((raw / st["norm"][j]) / (j + 1)).astype(np.float32)
     return None
 
 
-def _make_spectral(spec: ConfigSpec, n: int, d: int, seed: int, workers: int) -> np.ndarray:
+def _make_spectral(spec: ConfigSpec, n: int, d: int, seed: int, workers: int, rows=None) -> np.ndarray:
     chunks = list(_chunks(n))
     tasks = [(j, c, lo, hi, seed) for j in range(d) for (c, lo, hi) in chunks]
-    dots = _pool_map(_spectral_dot_task, tasks, workers)
+    dots = _pool_map(_spectral_dot_task, tasks, workers)   # column norms need every row
     nch = len(chunks)
     norm = np.empty(d)
     for j in range(d):
@@ -170,10 +190,11 @@ def _make_spectral(spec: ConfigSpec, n: int, d: int, seed: int, workers: int) ->
         for c in range(nch):          # fp64, chunk order
             ss += dots[j * nch + c]
         norm[j] = np.sqrt(ss)
-    out = _shared_array((n, d), np.float32)
-    _SHARED["spec"] = dict(out=out, norm=norm)
+    rlo, rhi = (0, n) if rows is None else rows
+    out = _shared_array((rhi - rlo, d), np.float32)
+    _SHARED["spec"] = dict(out=out, norm=norm, rows=(rlo, rhi))
     try:
-        _pool_map(_spectral_fill_task, tasks, workers)
+        _pool_map(_spectral_fill_task, [t for t in tasks if t[3] > rlo and t[2] < rhi], workers)
     finally:
         _SHARED.pop("spec", None)
     return out
@@ -181,17 +202,21 @@ def _make_spectral(spec: ConfigSpec, n: int, d: int, seed: int, workers: int) ->
 
 # ---- public -----------------------------------------------------------------------------
 def make_points(name: str, n: Optional[int] = None, seed: int = 0,
-                workers: Optional[int] = None) -> np.ndarray:
+                workers: Optional[int] = None, rows: Optional[Tuple[int, int]] = None) -> np.ndarray:
     """X (n x d, fp32, C-contiguous) for config ``name``.  ``n`` overrides the row count
-    (a prefix-compatible smaller instance of the same recipe, used for parity cases;
-    for ``spectral`` a smaller n changes the column norms, so it is a new instance of the
-    same distribution, not a prefix)."""
+    (a smaller instance of the same recipe, used for parity cases; for ``spectral`` a
+    smaller n changes the column norms, so it is a new instance of the same distribution,
+    not a prefix).  ``rows=(lo, hi)`` returns only those rows of the n-row matrix (a rank's
+    shard), byte-identical to slicing the full matrix."""
     spec = CONFIGS[name]
     n = spec.n if n is None else int(n)
     w = _workers(workers)
+    if rows is not None:
+        rows = (int(rows[0]), int(rows[1]))
+        assert 0 <= rows[0] <= rows[1] <= n
     if spec.kind == "mixture":
-        return _make_mixture(spec, n, seed, w)
-    return _make_spectral(spec, n, spec.d, seed, w)
+        return _make_mixture(spec, n, seed, w, rows)
+    return _make_spectral(spec, n, spec.d, seed, w, rows)
 
 
 def forgy_indices(n: int, k: int, seed: int = 0) -> np.ndarray:

