@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the MTI-pruned Lloyd's k-means hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--prune mti|none]
+    python bench.py --impl reference ...     # the fp64 CPU oracle as the reference arm
+
+A "step" is one full Lloyd iteration (S1 geometry/drift, S2 MTI assignment, S3 reduction +
+allreduce, S4 update, plus any re-bucketing the runtime decides) over the whole data set of
+the named config.  The first W iterations (iteration 1 is the dense no-bounds pass) are
+warm-up; the next K are timed.  Default workload: C3 (n = 65,608,366, d = 8, k = 100,
+spectral-embedding-shaped), the n = 66M configuration the metric is quoted on.
+
+Multi-GPU (torchrun): rows are sharded contiguously over ranks (strong scaling: the global
+data set is fixed); the library's NCCL communicator does one allreduce per iteration.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "k-means iters/s and effective point·centroid dists/s at n=66M; HBM GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=27)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--prune", default="mti", choices=["mti", "none"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stats-out", default=None)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def traffic_from_profile(cfg: str, prune: str):
+    p = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{prune}.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_oracle_rate(X, C0, n_full: int, k: int, sample_rows: int, iters: int):
+    """The fp64 oracle (oracle/, as it stands) on the first ``sample_rows`` rows: iteration 1
+    brute force untimed, then ``iters`` timed MTI iterations (oracle_mti_pass + block sums +
+    update).  Returns (full-workload iterations/s extrapolated by rows, seconds, threads)."""
+    import numpy as np
+    import oracle
+    Xs = np.ascontiguousarray(X[:sample_rows])
+    a, d1, _ = oracle.assign_brute(Xs, C0)
+    u = np.sqrt(d1)
+    sums, counts = oracle.cluster_sums(Xs, a, k)
+    C, _ = oracle.update(sums, counts, C0)
+    Cprev = C0
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        a, u, _, _, _ = oracle.mti_pass(Xs, C, Cprev, a, u)
+        sums, counts = oracle.cluster_sums(Xs, a, k)
+        Cprev, (C, _) = C, oracle.update(sums, counts, C)
+    dt = time.perf_counter() - t0
+    rate = iters / dt * (sample_rows / n_full)
+    return rate, dt, oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    import numpy as np
+    from synth import CONFIGS, make_config
+    if rank != 0:
+        return 0
+    spec = CONFIGS[args.config]
+    X, idx, _ = make_config(args.config)
+    C0 = X[idx].astype(np.float64)
+    sample = min(spec.n, 2_000_000 if spec.d <= 16 else 1_000_000)
+    if spec.k >= 1000:
+        sample = min(spec.n, 200_000)
+    # warm-up steps (untimed) then K timed oracle MTI iterations on the sample
+    cpu_oracle_rate(X, C0, spec.n, spec.k, sample, max(1, args.warmup))
+    rate, dt, cores = cpu_oracle_rate(X, C0, spec.n, spec.k, sample, args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "iters/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8(d) recipe, seed 0)",
+        "config": {"workload": f"{args.config}: n={spec.n}, d={spec.d}, k={spec.k}", "prune": "mti",
+                   "parallelism": "host cores (OpenMP)"},
+        "effective_dists_per_s": rate * spec.n * spec.k,
+        "cpu_baseline": {"value": rate, "unit": "iters/s", "cores": cores, "kind": "oracle",
+                         "sample": f"first {sample} rows of {args.config}, {args.steps} MTI iterations "
+                                   f"after 1 brute + {args.warmup} warm-up, extrapolated x{spec.n / sample:.2f} by rows"},
+        "e2e": {"value": rate, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    from synth import CONFIGS, make_points, forgy_indices
+    from paper_1902_09527_b200.dist import shard_bounds
+    spec = CONFIGS[args.config]
+    n, d, k = spec.n, spec.d, spec.k
+    lo, hi = shard_bounds(n, rank, world)
+    # generate before touching CUDA (fork pool)
+    t_gen = time.perf_counter()
+    X = make_points(args.config, rows=(lo, hi))
+    idx = forgy_indices(n, k)
+    if world == 1:
+        C0 = X[idx].astype(np.float64)
+    else:
+        C0 = None
+    t_gen = time.perf_counter() - t_gen
+
+    import torch
+    import torch.distributed as dist
+    from paper_1902_09527_b200 import KMeans, nccl_unique_id
+    from paper_1902_09527_b200.dist import broadcast_bytes, max_over_ranks
+
+    torch.cuda.set_device(local_rank)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl")
+        # Forgy rows live on different shards: gather them through the process group
+        rows = torch.zeros((k, d), dtype=torch.float64, device="cuda")
+        own = (idx >= lo) & (idx < hi)
+        if own.any():
+            rows[torch.from_numpy(np.nonzero(own)[0]).cuda()] = torch.from_numpy(
+                X[idx[own] - lo].astype(np.float64)).cuda()
+        dist.all_reduce(rows)
+        C0 = rows.cpu().numpy()
+        nccl_id = broadcast_bytes(nccl_unique_id() if rank == 0 else b"\0" * 128)
+
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    stream = torch.cuda.current_stream()
+    km = KMeans(Xd, C0, prune=args.prune, stream=stream.cuda_stream, rank=rank, world=world,
+                nccl_id=nccl_id, n_global=n)
+    for _ in range(args.warmup):
+        km.iterate()
+    launches0 = km.launch_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            km.iterate()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    ms_max = max_over_ranks(ms)
+    launches = km.launch_count - launches0
+    stats = km.stats()
+    timed = stats[args.warmup:args.warmup + args.steps]
+    assign_ms = [s["ms_assign"] for s in timed]
+    avg_assign = sum(assign_ms) / len(assign_ms)
+    bytes_per_row = 4 * d + 16 if args.prune == "mti" else 4 * d + 16
+    algo_bytes = (hi - lo) * bytes_per_row
+    peak, peak_src = load_peaks()
+    achieved = algo_bytes / (avg_assign * 1e-3) / 1e9
+    sse = km.sse()
+    km.close()
+    del Xd
+    torch.cuda.empty_cache()
+
+    iters_per_s = args.steps / (ms_max * 1e-3)
+    dists_computed = sum(s["dists"] for s in timed)
+    iter_bytes = n * bytes_per_row
+    line = {
+        "metric": METRIC, "value": iters_per_s, "unit": "iters/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 distances / f64 sums+centroids (exact mode)",
+        "data": "synthetic (SURVEY §8(d) recipe, seed 0; stands in for Friendster-8)",
+        "config": {"workload": f"{args.config}: n={n}, d={d}, k={k}, Forgy init, iterations "
+                               f"{args.warmup + 1}..{args.warmup + args.steps}",
+                   "prune": args.prune, "parallelism": f"rows sharded over {world} GPU(s)",
+                   "l2": f"inputs {n * 4 * d / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
+        "effective_dists_per_s": iters_per_s * n * k,
+        "dists_computed_per_s": dists_computed / (ms_max * 1e-3),
+        "hbm_gbs_step": iter_bytes * iters_per_s / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic_from_profile(args.config, args.prune),
+                     "kernel": "k_assign<MTI_REDUCE>" if args.prune == "mti" else "k_assign<DENSE_REDUCE>",
+                     "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": avg_assign,
+                     "peak_source": peak_src},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "final_sse": sse,
+        "gen_s": t_gen,
+    }
+    if args.stats_out and rank == 0:
+        json.dump(stats, open(args.stats_out, "w"), indent=1)
+
+    # ---- e2e: the public API end to end from pinned host memory -----------------------------
+    if not args.no_e2e:
+        Xh = torch.empty((hi - lo, d), dtype=torch.float32, pin_memory=True)
+        Xh.numpy()[:] = X
+        total_iters = args.warmup + args.steps
+        a_out = np.empty(hi - lo, np.int32)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nccl_id, n_global=n,
+                     device=local_rank)
+        for _ in range(total_iters):
+            km2.iterate()
+        a_out[:] = km2.assignments()
+        C_out = km2.centroids()
+        t_e2e = time.perf_counter() - t0
+        km2.close()
+        t_e2e = max_over_ranks(t_e2e)
+        line["e2e"] = {"value": total_iters / t_e2e, "unit": "iters/s",
+                       "h2d_bytes_per_step": (hi - lo) * d * 4 / total_iters,
+                       "d2h_bytes_per_step": ((hi - lo) * 4 + C_out.nbytes) / total_iters,
+                       "iterations": total_iters, "includes": "create(H2D) + all iterations + D2H a, C"}
+        del Xh
+    # ---- CPU baseline: the oracle on the host cores (rank 0, N=1 only) ------------------------
+    if world == 1 and not args.no_cpu_baseline:
+        sample = min(n, 2_000_000 if d <= 16 else 1_000_000)
+        if k >= 1000:
+            sample = min(n, 200_000)
+        it = 3
+        rate, dt, cores = cpu_oracle_rate(X, C0, n, k, sample, it)
+        line["cpu_baseline"] = {"value": rate, "unit": "iters/s", "cores": cores, "kind": "oracle",
+                                "sample": f"first {sample} rows of {args.config}, {it} MTI iterations "
+                                          f"after 1 brute ({dt:.1f} s), extrapolated x{n / sample:.2f} by rows"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -75,6 +75,8 @@ typedef struct km_iter_stats {
     int64_t dists;     /* point-centroid distances evaluated under the MTI semantics (global) */
     int64_t clause1;   /* points skipped by clause 1 (global) */
     int64_t refined;   /* points re-evaluated in fp64 by exact mode (global) */
+    int64_t walk_steps; /* warp-steps of the MTI candidate walk (global); lane efficiency =
+                           (dists - points tightened) / (32 * walk_steps) */
     int32_t empty;     /* clusters with no points after this iteration's assignment */
     int32_t resorted;  /* 1 if the rows were re-bucketed after this iteration's pass */
     float ms_iter;     /* device time of the whole iteration (CUDA events, this rank) */

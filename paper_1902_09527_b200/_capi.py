@@ -30,7 +30,7 @@ class KmOptions(ct.Structure):
 
 class KmIterStats(ct.Structure):
     _fields_ = [("changed", ct.c_int64), ("dists", ct.c_int64), ("clause1", ct.c_int64),
-                ("refined", ct.c_int64), ("empty", ct.c_int32), ("resorted", ct.c_int32),
+                ("refined", ct.c_int64), ("walk_steps", ct.c_int64), ("empty", ct.c_int32), ("resorted", ct.c_int32),
                 ("ms_iter", ct.c_float), ("ms_assign", ct.c_float), ("ms_sort", ct.c_float),
                 ("ms_comm", ct.c_float)]
 

@@ -92,8 +92,8 @@ NcclApi *nccl()
 }
 
 struct HostStat {
-    unsigned long long local[4];   // changed, dists, clause1, refined (this rank)
-    unsigned long long global[4];  // after allreduce
+    unsigned long long local[8];   // changed, dists, clause1, refined, walk_steps (this rank)
+    unsigned long long global[8];  // after allreduce
     int empty;
     int pad;
 };
@@ -131,6 +131,7 @@ struct km_ctx {
     // sort scratch
     uint32_t *keys = nullptr, *hist = nullptr, *totals = nullptr, *base = nullptr;
     int Q = 1, NB = 0, ntiles = 0, tile_rows = 32768;
+    int ks = 0;                     // NL row stride
     // centroid state
     double *C = nullptr, *Cprev = nullptr;
     float *Cneg = nullptr, *f = nullptr, *s = nullptr;
@@ -138,7 +139,10 @@ struct km_ctx {
     // per-iteration scratch (zeroed by one memset): acc | counters | empty, eps_bits, work[2]
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
-    double *acc = nullptr;
+    double *acc = nullptr;          // k x (DP+1) reduced sums | counts (allreduce buffer)
+    double *acc_part = nullptr;     // grid x k x (DP+1) per-CTA partials
+    int part_grid = 0;
+    int nslab = 0;                  // number of partial slabs (= SM count)
     unsigned long long *counters = nullptr, *counters_g = nullptr;
     int *empty = nullptr, *work = nullptr;
     unsigned *eps_bits = nullptr;
@@ -168,6 +172,7 @@ km_status prep(km_ctx *c)
     p.d = c->d;
     p.DP = c->DP;
     p.sortN = std::max(2, next_pow2(c->k));
+    p.ks = c->ks;
     p.Cneg = c->Cneg;
     p.f = c->f;
     p.s = c->s;
@@ -190,13 +195,15 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
     p.Cneg = c->Cneg;
     p.C64 = c->C;
     p.NL = c->NL;
+    p.ks = c->ks;
     p.f = c->f;
     p.s = c->s;
     p.eps = reinterpret_cast<const float *>(c->eps_bits);
     p.g_up = c->g_up;
     p.g_dn = c->g_dn;
     p.count_changed = c->t > 1;
-    p.acc = c->acc;
+    p.acc = c->acc_part;
+    p.nslab = c->nslab;
     p.counters = c->counters;
     p.work = c->work + work_slot;
     return p;
@@ -207,6 +214,11 @@ km_status launch_assign(km_ctx *c, int mode, int work_slot)
     km::AssignParams p = assign_params(c, work_slot);
     KM_CUDA(km::launch_assign(mode, c->DP, c->csmem, p, c->grid_assign[mode], c->st));
     c->launches += 1;
+    if (mode != km::MODE_DENSE) {
+        KM_CUDA(km::launch_partials_reduce(c->acc_part, c->nslab,
+                                           (int64_t)c->k * (c->DP + 1), c->acc, c->st));
+        c->launches += 1;
+    }
     return KM_OK;
 }
 
@@ -217,7 +229,7 @@ km_status resort(km_ctx *c)
     p.X = c->X[o]; p.a = c->a[o]; p.u = c->u[o]; p.perm = c->perm[o];
     p.X2 = c->X[nw]; p.a2 = c->a[nw]; p.u2 = c->u[nw]; p.perm2 = c->perm[nw];
     p.keys = c->keys; p.hist = c->hist; p.totals = c->totals; p.base = c->base;
-    p.NL = c->NL; p.s = c->s;
+    p.NL = c->NL; p.s = c->s; p.ks = c->ks;
     p.n = c->n; p.k = c->k; p.DP = c->DP;
     p.Q = c->prune == KM_PRUNE_MTI ? c->Q : 1;
     p.NB = c->k * p.Q;
@@ -234,7 +246,7 @@ km_status resort(km_ctx *c)
 km_status allreduce(km_ctx *c)
 {
     if (c->world <= 1) {
-        KM_CUDA(cudaMemcpyAsync(c->counters_g, c->counters, 4 * sizeof(unsigned long long),
+        KM_CUDA(cudaMemcpyAsync(c->counters_g, c->counters, 8 * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToDevice, c->st));
         return KM_OK;
     }
@@ -244,7 +256,7 @@ km_status allreduce(km_ctx *c)
     N->GroupStart();
     r = N->AllReduce(c->acc, c->acc, (size_t)c->k * (c->DP + 1), ncclFloat64, ncclSum, c->comm, c->st);
     if (r == ncclSuccess)
-        r = N->AllReduce(c->counters, c->counters_g, 4, ncclUint64, ncclSum, c->comm, c->st);
+        r = N->AllReduce(c->counters, c->counters_g, 8, ncclUint64, ncclSum, c->comm, c->st);
     ncclResult_t r2 = N->GroupEnd();
     if (r != ncclSuccess) return fail(KM_ENCCL, "ncclAllReduce: %s", N->GetErrorString(r));
     if (r2 != ncclSuccess) return fail(KM_ENCCL, "ncclGroupEnd: %s", N->GetErrorString(r2));
@@ -281,6 +293,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     }
     KM_CUDA(cudaEventRecord(ev[1], c->st));
     KM_CUDA(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, c->st));
+    KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
     KM_TRY(prep(c));
     KM_CUDA(cudaEventRecord(ev[2], c->st));
     if (first) {
@@ -300,9 +313,9 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     KM_CUDA(cudaEventRecord(ev[5], c->st));
     KM_CUDA(km::launch_update(c->acc, c->C, c->Cprev, c->k, c->d, c->DP, c->empty, c->st));
     c->launches += 1;
-    KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 4 * sizeof(unsigned long long),
+    KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, c->st));
-    KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 4 * sizeof(unsigned long long),
+    KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 8 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, c->st));
     KM_CUDA(cudaMemcpyAsync(&c->hstat->empty, c->empty, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     KM_CUDA(cudaEventRecord(ev[6], c->st));
@@ -319,6 +332,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     }
     rec.clause1 = (int64_t)h->global[2];
     rec.refined = (int64_t)h->global[3];
+    rec.walk_steps = (int64_t)h->global[4];
     rec.empty = h->empty;
     rec.resorted = sorted_now;
     rec.ms_assign = elapsed(ev[2], ev[3]);
@@ -339,7 +353,7 @@ void free_all(km_ctx *c)
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
     cudaFree(c->NL); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
-    cudaFree(c->counters_g);
+    cudaFree(c->counters_g); cudaFree(c->acc_part);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
     if (c->comm) { NcclApi *N = nccl(); if (N) N->CommDestroy(c->comm); }
@@ -398,17 +412,19 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     KM_TRY(dalloc(&c->Cneg, (size_t)k * DP));
     KM_TRY(dalloc(&c->f, (size_t)k));
     KM_TRY(dalloc(&c->s, (size_t)k));
-    KM_TRY(dalloc(&c->NL, (size_t)k * std::max(1, k - 1)));
+    c->ks = (k + 1) & ~1;
+    KM_TRY(dalloc(&c->NL, (size_t)(k + 1) * c->ks));   // + one spare row (prefetch slack)
+    KM_CUDA(cudaMemset(c->NL, 0, (size_t)(k + 1) * c->ks * sizeof(uint64_t)));
     const size_t acc_bytes = (size_t)k * (DP + 1) * sizeof(double);
-    c->scratch_bytes = acc_bytes + 4 * sizeof(unsigned long long) + 8 * sizeof(int);
+    c->scratch_bytes = acc_bytes + 8 * sizeof(unsigned long long) + 8 * sizeof(int);
     KM_CUDA(cudaMalloc(&c->scratch, c->scratch_bytes));
     c->acc = static_cast<double *>(c->scratch);
     c->counters = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->scratch) + acc_bytes);
-    int *ints = reinterpret_cast<int *>(c->counters + 4);
+    int *ints = reinterpret_cast<int *>(c->counters + 8);
     c->empty = ints + 0;
     c->eps_bits = reinterpret_cast<unsigned *>(ints + 1);
     c->work = ints + 2;   // two work counters
-    KM_TRY(dalloc(&c->counters_g, 4));
+    KM_TRY(dalloc(&c->counters_g, 8));
     KM_TRY(dalloc(&c->sse_buf, 1));
     KM_CUDA(cudaMallocHost(&c->hstat, sizeof(HostStat)));
     // points -> private padded copy
@@ -432,7 +448,12 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         KM_CUDA(cudaStreamSynchronize(c->st));
         if (flag) return fail(KM_ENONFINITE, "points contain NaN or Inf");
     }
-    for (int m = 0; m < 4; ++m) c->grid_assign[m] = km::assign_grid(m, DP, c->csmem, k, c->num_sms);
+    for (int m = 0; m < 4; ++m) {
+        c->grid_assign[m] = km::assign_grid(m, DP, c->csmem, k, c->num_sms);
+        c->part_grid = std::max(c->part_grid, c->grid_assign[m]);
+    }
+    c->nslab = std::min(c->part_grid, c->num_sms);
+    KM_TRY(dalloc(&c->acc_part, (size_t)c->nslab * k * (DP + 1)));
     if (c->world > 1) {
         NcclApi *N = nccl();
         if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable (world=%d)", c->world);

@@ -12,6 +12,8 @@
 
 #include <math.h>
 
+#include <algorithm>
+
 namespace km {
 
 // ---------------------------------------------------------------------------------------
@@ -40,14 +42,38 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c)
 // Squared distance ||x - c||^2 in fp32, direct-difference form: t = x + (-c) (IEEE x - c),
 // squares accumulated with fma in four interleaved partial sums.  Relative error of the
 // result <= (DP/4 + 4) * 2^-24 (+O(2^-48)); DESIGN.md "Exact mode" bounds sqrt of it by gamma.
+__device__ __forceinline__ float4 lds128(uint32_t addr)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
+// Centroid row source: shared memory (32-bit shared-window address) or global (__ldg).
+template <bool SMEM> struct CRow;
+template <> struct CRow<true> {
+    uint32_t base;
+    __device__ __forceinline__ float4 ld(int c, int DP, int j) const
+    {
+        return lds128(base + (uint32_t)((c * DP + j) * 4));
+    }
+};
+template <> struct CRow<false> {
+    const float *base;
+    __device__ __forceinline__ float4 ld(int c, int DP, int j) const
+    {
+        return __ldg(reinterpret_cast<const float4 *>(base + (int64_t)c * DP + j));
+    }
+};
+
 template <int DP, bool SMEM>
-__device__ __forceinline__ float dist2(const float (&x)[DP], const float *cneg)
+__device__ __forceinline__ float dist2(const float (&x)[DP], const CRow<SMEM> &cr, int cidx)
 {
     float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < DP; j += 4) {
-        float4 c = SMEM ? *reinterpret_cast<const float4 *>(cneg + j)
-                        : __ldg(reinterpret_cast<const float4 *>(cneg + j));
+        float4 c = cr.ld(cidx, DP, j);
         float2 t0 = add2(make_float2(x[j], x[j + 1]), make_float2(c.x, c.y));
         float2 t1 = add2(make_float2(x[j + 2], x[j + 3]), make_float2(c.z, c.w));
         acc0 = fma2(t0, t0, acc0);
@@ -68,6 +94,7 @@ __device__ __forceinline__ float lower_d(float q, float g_dn, float eps)
     return fmaxf(0.f, __fsub_rd(__fmul_rd(__fsqrt_rd(q), g_dn), eps));
 }
 
+constexpr uint64_t kSentinel = 0xffffffff00000000ull;   // h = NaN (never < u), c = 0
 __device__ __forceinline__ float key_h(uint64_t key) { return __uint_as_float((uint32_t)(key >> 32)); }
 __device__ __forceinline__ int key_c(uint64_t key) { return (int)(uint32_t)(key & 0xffffffffull); }
 
@@ -89,7 +116,7 @@ __device__ __noinline__ int refine64(const float *xrow, int d, const double *C64
     };
     if (nl) {
         eval(A);
-        for (int j = 0; j < k - 1; ++j) {
+        for (int j = 0;; ++j) {          // row ends with a sentinel whose h is NaN
             uint64_t key = nl[j];
             if (!(key_h(key) < ut)) break;
             eval(key_c(key));
@@ -202,7 +229,9 @@ __device__ __forceinline__ void reduce_batch(RunAcc<DP> &ra, const float (&x)[DP
     ra.cnt += __popc(mR);
     if (valid && !in) {      // lane leaves the warp's run cluster: direct fp64 RED
         double *row = acc + (int64_t)anew * (DP + 1);
-        for (int j = 0; j < d; ++j) atomicAdd(row + j, (double)x[j]);
+#pragma unroll
+        for (int j = 0; j < DP; ++j)          // compile-time indices keep x in registers
+            if (j < d) atomicAdd(row + j, (double)x[j]);
         atomicAdd(row + DP, 1.0);
     }
 }
@@ -233,7 +262,15 @@ k_assign(AssignParams p)
             for (int i = threadIdx.x; i < k; i += blockDim.x) { sF[i] = p.f[i]; sS[i] = p.s[i]; }
     }
     __syncthreads();
-    const float *Cn = CSMEM ? sC : p.Cneg;
+    CRow<CSMEM> Cn;
+    if constexpr (CSMEM) {
+        uint32_t b = (uint32_t)__cvta_generic_to_shared(sC);
+        asm volatile("mov.u32 %0, %0;" : "+r"(b));   // keep in a register (no re-materialisation)
+        Cn.base = b;
+    }
+    else Cn.base = p.Cneg;
+    // this CTA's private partial-sum slab: fp64 REDs from different CTAs never contend
+    double *acc = p.acc + (int64_t)(blockIdx.x % p.nslab) * k * (DP + 1);
     const float eps = ASSIGN ? *p.eps : 0.f;
     const int lane = threadIdx.x & (kWarp - 1);
     const int64_t n = p.n;
@@ -241,105 +278,138 @@ k_assign(AssignParams p)
     RunAcc<DP> ra;
     ra.clear();
     unsigned long long c_changed = 0, c_dists = 0, c_clause1 = 0, c_refined = 0;
+    unsigned steps = 0;
+    const int ks = p.ks;                        // NL row stride (even, >= k)
 
-    for (;;) {
-        int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(p.work, 1);
-        chunk = __shfl_sync(kFull, chunk, 0);
-        const int64_t row0 = (int64_t)chunk * kChunkRows;
-        if (row0 >= n) break;
-#pragma unroll 1
-        for (int b = 0; b < kChunkRows / kWarp; ++b) {
-            const int64_t row = row0 + b * kWarp + lane;
-            const bool valid = row < n;
-            if (!__any_sync(kFull, valid)) break;
-            float x[DP];
-            {
-                const float4 *xr = reinterpret_cast<const float4 *>(p.X + (valid ? row : 0) * DP);
+    // Row stream of this warp: chunks of kChunkRows rows claimed from a global counter (one
+    // chunk ahead), batches of 32 rows (one per lane); the next batch's x, a, u are loaded
+    // before the current batch is processed, so HBM latency overlaps the distance work.
+    constexpr int kBatches = kChunkRows / kWarp;
+    auto claim = [&]() -> int64_t {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(p.work, 1);
+        return (int64_t)__shfl_sync(kFull, c, 0) * kChunkRows;
+    };
+    int64_t chunk_row = claim(), ahead_row = claim();
+    int b = 0;
+    float nx[DP];
+    int na = 0;
+    float nu = 0.f;
+    auto load = [&](int64_t row) {
+        const bool v = row < n;
+        const float4 *xr = reinterpret_cast<const float4 *>(p.X + (v ? row : 0) * DP);
 #pragma unroll
-                for (int j = 0; j < DP / 4; ++j) {
-                    float4 t = valid ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    x[4 * j] = t.x; x[4 * j + 1] = t.y; x[4 * j + 2] = t.z; x[4 * j + 3] = t.w;
-                }
-            }
-            const int aold = valid ? p.a[row] : 0;
-            int anew = aold;
-            if (ASSIGN) {
-                float unew = 0.f;
-                bool active = valid;
-                if (PRUNE) {
-                    const float uu = valid ? __fadd_ru(p.u[row], sF[aold]) : 0.f;  // u += f(a)
-                    const bool c1 = valid && uu <= sS[aold];                       // clause 1
-                    c_clause1 += c1;
-                    active = valid && !c1;
-                    unew = uu;
-                }
-                if (__any_sync(kFull, active)) {
-                    float bq = INFINITY, q2 = INFINITY, ut = 0.f;
-                    int bc = aold, ns = 0;
-                    if (DENSE) {
-#pragma unroll 1
-                        for (int c = 0; c < k; ++c) {
-                            const float q = dist2<DP, CSMEM>(x, Cn + c * DP);
-                            if (q < bq) { q2 = bq; bq = q; bc = c; }
-                            else if (q < q2) { q2 = q; }
-                        }
-                        ns = k;
-                    } else {
-                        // group the warp by assigned cluster; each group walks its cluster's
-                        // neighbour list (ascending H) with broadcast centroid reads
-                        unsigned rem = __ballot_sync(kFull, active);
-                        while (rem) {
-                            const int A = __shfl_sync(kFull, aold, __ffs(rem) - 1);
-                            const bool mine = active && aold == A;
-                            rem &= ~__ballot_sync(kFull, mine);
-                            if (mine) {                         // tighten: U(u) = d(x, C[a])
-                                bq = dist2<DP, CSMEM>(x, Cn + A * DP);
-                                bc = A;
-                                ut = upper_d(bq, p.g_up, eps);
-                                ns = 1;
-                            }
-                            const uint64_t *nl = p.NL + (int64_t)A * (k - 1);
-#pragma unroll 1
-                            for (int j = 0; j < k - 1; ++j) {
-                                const uint64_t key = __ldg(nl + j);
-                                const bool go = mine && key_h(key) < ut;   // clauses 2/3
-                                if (!__any_sync(kFull, go)) break;
-                                if (go) {
-                                    const int c = key_c(key);
-                                    const float q = dist2<DP, CSMEM>(x, Cn + c * DP);
-                                    ++ns;
-                                    if (q < bq || (q == bq && c < bc)) { q2 = bq; bq = q; bc = c; }
-                                    else if (q < q2) { q2 = q; }
-                                }
-                            }
-                        }
-                    }
-                    if (active) {
-                        const float ub = upper_d(bq, p.g_up, eps);
-                        const bool amb = q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub;
-                        if (amb) {
-                            anew = refine64(p.X + row * DP, p.d, p.C64, k, aold,
-                                            DENSE ? nullptr : p.NL + (int64_t)aold * (k - 1),
-                                            ut, &unew);
-                            ++c_refined;
-                        } else {
-                            anew = bc;
-                            unew = ub;
-                        }
-                        c_dists += (unsigned long long)ns;
-                    }
-                }
-                if (valid) {
-                    p.a[row] = anew;
-                    p.u[row] = unew;
-                    if (p.count_changed) c_changed += (anew != aold);
-                }
-            }
-            if (REDUCE) reduce_batch<DP>(ra, x, anew, valid, p.acc, p.d, lane);
+        for (int j = 0; j < DP / 4; ++j) {
+            float4 t = v ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+            nx[4 * j] = t.x; nx[4 * j + 1] = t.y; nx[4 * j + 2] = t.z; nx[4 * j + 3] = t.w;
         }
+        na = v ? __ldg(p.a + row) : 0;
+        nu = (v && PRUNE) ? __ldg(p.u + row) : 0.f;
+    };
+    load(chunk_row + lane);
+
+    while (chunk_row < n) {
+        const int64_t row = chunk_row + b * kWarp + lane;
+        const bool valid = row < n;
+        float x[DP];
+#pragma unroll
+        for (int j = 0; j < DP; ++j) x[j] = nx[j];
+        const int aold = na;
+        const float uold = nu;
+        // advance the stream and prefetch the next batch
+        if (++b == kBatches || chunk_row + b * kWarp >= n) {
+            b = 0;
+            chunk_row = ahead_row;
+            ahead_row = chunk_row < n ? claim() : ahead_row;
+        }
+        if (chunk_row < n) load(chunk_row + b * kWarp + lane);
+
+        int anew = aold;
+        if (ASSIGN) {
+            float unew = 0.f;
+            bool active = valid;
+            if (PRUNE) {
+                const float uu = valid ? __fadd_ru(uold, sF[aold]) : 0.f;  // u += f(a)
+                const bool c1 = valid && uu <= sS[aold];                   // clause 1
+                c_clause1 += c1;
+                active = valid && !c1;
+                unew = uu;
+            }
+            if (__any_sync(kFull, active)) {
+                float bq = INFINITY, q2 = INFINITY, ut = 0.f;
+                int bc = aold, ns = 0;
+                if (DENSE) {
+#pragma unroll 4
+                    for (int c = 0; c < k; ++c) {
+                        const float q = dist2<DP, CSMEM>(x, Cn, c);
+                        q2 = fminf(q2, fmaxf(q, bq));
+                        bc = q < bq ? c : bc;
+                        bq = fminf(q, bq);
+                    }
+                    ns = k;
+                } else {
+                    // Every lane walks its own cluster's neighbour list (ascending H) in
+                    // lockstep, two candidates per step; rows are bucketed by cluster, so
+                    // lanes mostly share the list and centroid reads are broadcasts.  Steps =
+                    // the longest walk in the warp, whatever the mix of clusters.
+                    if (active) {                           // tighten: U(u) = d(x, C[a])
+                        bq = dist2<DP, CSMEM>(x, Cn, aold);
+                        bc = aold;
+                        ut = upper_d(bq, p.g_up, eps);
+                        ns = 1;
+                    }
+                    // NL rows (stride ks, even) end with sentinels (h = NaN, c = 0) and the
+                    // array has a spare row, so pair loads never leave the allocation and
+                    // every key's c is a valid centroid index, even past a lane's own walk.
+                    const uint64_t *nl = p.NL + (int64_t)aold * ks;
+                    bool walking = active;
+                    ulonglong2 kp = __ldg(reinterpret_cast<const ulonglong2 *>(nl));
+                    for (int j = 0;; j += 2) {
+                        const bool w0 = walking && key_h(kp.x) < ut;   // clauses 2/3
+                        const bool w1 = w0 && key_h(kp.y) < ut;
+                        if (!__any_sync(kFull, w0)) break;
+                        steps += 2;
+                        const ulonglong2 np = __ldg(reinterpret_cast<const ulonglong2 *>(nl + j + 2));
+                        const int c0 = key_c(kp.x), c1 = key_c(kp.y);
+                        float q0 = dist2<DP, CSMEM>(x, Cn, c0);
+                        float q1 = dist2<DP, CSMEM>(x, Cn, c1);
+                        q0 = w0 ? q0 : INFINITY;
+                        q1 = w1 ? q1 : INFINITY;
+                        ns += (int)w0 + (int)w1;
+                        // fp32 ties are resolved later: equal q makes q2 == bq -> refinement
+                        q2 = fminf(q2, fmaxf(q0, bq));
+                        bc = q0 < bq ? c0 : bc;
+                        bq = fminf(q0, bq);
+                        q2 = fminf(q2, fmaxf(q1, bq));
+                        bc = q1 < bq ? c1 : bc;
+                        bq = fminf(q1, bq);
+                        walking = w1;
+                        kp = np;
+                    }
+                }
+                if (active) {
+                    const float ub = upper_d(bq, p.g_up, eps);
+                    const bool amb = q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub;
+                    if (amb) {
+                        anew = refine64(p.X + row * DP, p.d, p.C64, k, aold,
+                                        DENSE ? nullptr : p.NL + (int64_t)aold * ks, ut, &unew);
+                        ++c_refined;
+                    } else {
+                        anew = bc;
+                        unew = ub;
+                    }
+                    c_dists += (unsigned long long)ns;
+                }
+            }
+            if (valid) {
+                p.a[row] = anew;
+                p.u[row] = unew;
+                if (p.count_changed) c_changed += (anew != aold);
+            }
+        }
+        if (REDUCE) reduce_batch<DP>(ra, x, anew, valid, acc, p.d, lane);
     }
-    if (REDUCE) ra.flush(p.acc, p.d, lane);
+    if (REDUCE) ra.flush(acc, p.d, lane);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         c_changed += __shfl_xor_sync(kFull, c_changed, o);
@@ -352,6 +422,7 @@ k_assign(AssignParams p)
         if (c_dists) atomicAdd(p.counters + 1, c_dists);
         if (c_clause1) atomicAdd(p.counters + 2, c_clause1);
         if (c_refined) atomicAdd(p.counters + 3, c_refined);
+        if (steps) atomicAdd(p.counters + 4, (unsigned long long)steps);   // warp-uniform count
     }
 }
 
@@ -499,8 +570,8 @@ __global__ void k_prep(PrepParams p)
         }
     }
     __syncthreads();
-    uint64_t *nl = p.NL + (int64_t)c * (k - 1);
-    for (int j = threadIdx.x; j < k - 1; j += blockDim.x) nl[j] = keys[j];
+    uint64_t *nl = p.NL + (int64_t)c * p.ks;     // k - 1 neighbours, then sentinels (h = NaN, c = 0)
+    for (int j = threadIdx.x; j < p.ks; j += blockDim.x) nl[j] = j < k - 1 ? keys[j] : kSentinel;
     if (threadIdx.x == 0) p.s[c] = k > 1 ? __uint_as_float((uint32_t)(keys[0] >> 32)) : INFINITY;
 }
 
@@ -508,6 +579,33 @@ cudaError_t launch_prep(const PrepParams &p, cudaStream_t st)
 {
     size_t sm = (size_t)p.sortN * sizeof(uint64_t);
     k_prep<<<p.k, 256, sm, st>>>(p);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// S3 final step: acc[e] = sum over CTAs g (in order) of part[g][e]
+__global__ void __launch_bounds__(1024) k_partials_reduce(const double *part, int parts, int64_t elems, double *acc)
+{
+    // block = 32 elements x 32 warps; warp w sums parts w, w+32, ... then a fixed-order tree
+    __shared__ double red[32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (e < elems)
+        for (int g = w; g < parts; g += 32) s += part[(int64_t)g * elems + e];
+    red[w][lane] = s;
+    __syncthreads();
+    if (w == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 32; ++i) t += red[i][lane];
+        if (e < elems) acc[e] = t;
+    }
+}
+
+cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems, double *acc,
+                                   cudaStream_t st)
+{
+    k_partials_reduce<<<(unsigned)((elems + 31) / 32), 1024, 0, st>>>(part, parts, elems, acc);
     return cudaGetLastError();
 }
 
@@ -537,10 +635,10 @@ cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, in
 // Re-bucketing (counting sort by bucket = a * Q + prefix class).  The prefix length
 // p = #{c' : H[a][c'] < u} is the number of candidates the point would evaluate; rows of a
 // bucket therefore have similar walk lengths, which keeps warp lanes busy.
-__device__ __forceinline__ uint32_t bucket_of(int a, float u, const uint64_t *NL, int k, int Q)
+__device__ __forceinline__ uint32_t bucket_of(int a, float u, const uint64_t *NL, int k, int ks, int Q)
 {
     if (Q == 1) return (uint32_t)a;
-    const uint64_t *nl = NL + (int64_t)a * (k - 1);
+    const uint64_t *nl = NL + (int64_t)a * ks;
     int lo = 0, hi = k - 1;
     while (lo < hi) {
         int mid = (lo + hi) >> 1;
@@ -563,7 +661,7 @@ __global__ void k_sort_keys(SortParams p)
     int64_t r1 = r0 + p.tile_rows;
     if (r1 > p.n) r1 = p.n;
     for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        uint32_t b = bucket_of(p.a[r], p.u[r], p.NL, p.k, p.Q);
+        uint32_t b = bucket_of(p.a[r], p.u[r], p.NL, p.k, p.ks, p.Q);
         p.keys[r] = b;
         atomicAdd(&sh[b], 1u);
     }

@@ -7,7 +7,8 @@
 //   a, u   int32[n], fp32[n]   assignment and MTI upper bound, same row order as X
 //   perm   int32[n]            caller row index of each stored row
 //   Cneg   k x DP fp32         -fp32(C) (negated so x + (-c) is the IEEE x - c), zero padded
-//   NL     k x (k-1) uint64    per centroid c: (H[c][c'] as fp32 bits << 32 | c'), ascending
+//   NL     k x ks uint64       per centroid c: (H[c][c'] as fp32 bits << 32 | c'), ascending,
+//                               k-1 neighbours then sentinels (h = NaN, c = 0); ks = k rounded to even
 //   f, s   fp32[k]             drift (rounded up) and 1/2 nearest-centroid distance (rounded down)
 //   acc    k x (DP+1) fp64     per-cluster sums (DP slots, padded ones stay 0) and count
 #pragma once
@@ -37,24 +38,26 @@ struct AssignParams {
     int32_t d, k;
     const float *Cneg;     // k x DP
     const double *C64;     // k x d master centroids of this pass
-    const uint64_t *NL;    // k x (k-1)
+    const uint64_t *NL;    // k x ks (k-1 neighbours, then sentinels; + one spare row)
+    int32_t ks;            // NL row stride: k rounded up to even
     const float *f;        // k
     const float *s;        // k
     const float *eps;      // device scalar: eps_C (rounded up)
     float g_up, g_dn;      // 1 + gamma (rounded up), 1 - gamma (rounded down)
     int32_t count_changed; // 1: count a_new != a_old
-    double *acc;           // k x (DP+1)
-    unsigned long long *counters;  // [0] changed [1] dists [2] clause1 [3] refined
+    double *acc;           // partial-sum slabs: nslab x k x (DP+1) (zeroed before launch)
+    int32_t nslab;         // CTA b accumulates into slab b % nslab
+    unsigned long long *counters;  // [0] changed [1] dists [2] clause1 [3] refined [4] walk warp-steps
     int *work;             // dynamic chunk counter (zeroed before launch)
 };
 
 struct PrepParams {
     const double *C;       // k x d (centroids of the coming pass)
     const double *Cprev;   // k x d (centroids of the previous pass)
-    int32_t k, d, DP, sortN;
+    int32_t k, d, DP, sortN, ks;
     float *Cneg;           // k x DP
     float *f, *s;          // k
-    uint64_t *NL;          // k x (k-1)
+    uint64_t *NL;          // k x k
     unsigned *eps_bits;    // fp32 bits of eps_C (atomicMax; zeroed before launch)
 };
 
@@ -67,6 +70,7 @@ struct SortParams {
     uint32_t *base;        // NB
     const uint64_t *NL; const float *s;
     int64_t n;
+    int32_t ks;
     int32_t k, DP, Q, NB, ntiles, tile_rows;
 };
 
@@ -76,6 +80,8 @@ cudaError_t launch_assign(int mode, int DP, bool csmem, const AssignParams &p, i
                           cudaStream_t st);
 int assign_grid(int mode, int DP, bool csmem, int k, int num_sms);
 size_t assign_smem(int DP, bool csmem, int k);
+cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems, double *acc,
+                                  cudaStream_t st);
 cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, int d, int DP,
                           int *empty, cudaStream_t st);
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches);
