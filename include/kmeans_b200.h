@@ -55,6 +55,12 @@ enum { KM_PRUNE_MTI = 0, KM_PRUNE_NONE = 1 };
  * whenever the points reassigned since the last sort exceed resort_fraction * n_local. */
 enum { KM_RESORT_AUTO = 0, KM_RESORT_NEVER = 1, KM_RESORT_ALWAYS = 2 };
 
+/* Candidate-evaluation engine of the MTI pass.  AUTO uses the
+ * tcgen05 TF32x3 tensor-core kernel when d pads to 8, 16 or 32, else the CUDA-core kernel;
+ * both give the same (exact-mode) assignments.  Iteration 1 and KM_PRUNE_NONE always use
+ * the CUDA-core dense kernel. */
+enum { KM_ENGINE_AUTO = 0, KM_ENGINE_CUDA_CORE = 1, KM_ENGINE_TENSOR = 2 };
+
 typedef struct km_options {
     int32_t device;            /* CUDA device ordinal the context lives on */
     void *stream;              /* cudaStream_t, borrowed; NULL = the context creates its own */
@@ -67,7 +73,8 @@ typedef struct km_options {
     int32_t points_on_host;    /* 1 = points pointer is host memory (pinned preferred); copied at create */
     int32_t resort_policy;     /* KM_RESORT_* */
     float resort_fraction;     /* AUTO threshold, default 0.10 */
-    int32_t reserved[8];
+    int32_t engine;            /* KM_ENGINE_* (default AUTO) */
+    int32_t reserved[7];
 } km_options;
 
 typedef struct km_iter_stats {

@@ -15,6 +15,7 @@ SO_PATH = os.path.join(_PKG, "libkmeans_b200.so")
 KM_OK, KM_EARG, KM_ENONFINITE, KM_ECUDA, KM_ENCCL, KM_ENOMEM, KM_ESTATE = range(7)
 KM_PRUNE_MTI, KM_PRUNE_NONE = 0, 1
 KM_RESORT_AUTO, KM_RESORT_NEVER, KM_RESORT_ALWAYS = 0, 1, 2
+KM_ENGINE_AUTO, KM_ENGINE_CUDA_CORE, KM_ENGINE_TENSOR = 0, 1, 2
 STATUS_NAMES = {0: "KM_OK", 1: "KM_EARG", 2: "KM_ENONFINITE", 3: "KM_ECUDA", 4: "KM_ENCCL",
                 5: "KM_ENOMEM", 6: "KM_ESTATE"}
 
@@ -25,7 +26,7 @@ class KmOptions(ct.Structure):
                 ("nccl_unique_id", ct.c_uint8 * 128), ("n_global", ct.c_int64),
                 ("check_finite", ct.c_int32), ("points_on_host", ct.c_int32),
                 ("resort_policy", ct.c_int32), ("resort_fraction", ct.c_float),
-                ("reserved", ct.c_int32 * 8)]
+                ("engine", ct.c_int32), ("reserved", ct.c_int32 * 7)]
 
 
 class KmIterStats(ct.Structure):

@@ -136,6 +136,9 @@ struct km_ctx {
     double *C = nullptr, *Cprev = nullptr;
     float *Cneg = nullptr, *f = nullptr, *s = nullptr;
     uint64_t *NL = nullptr;
+    float *Bpre = nullptr, *cc = nullptr;   // tensor-core operand rows / |C|^2
+    bool use_tc = false;
+    int tc_W = 0, tc_cols = 0, tc_grid = 0;
     // per-iteration scratch (zeroed by one memset): acc | counters | empty, eps_bits, work[2]
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -177,6 +180,8 @@ km_status prep(km_ctx *c)
     p.f = c->f;
     p.s = c->s;
     p.NL = c->NL;
+    p.Bpre = c->Bpre;
+    p.cc = c->cc;
     p.eps_bits = c->eps_bits;
     KM_CUDA(km::launch_prep(p, c->st));
     c->launches += 1;
@@ -206,13 +211,20 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
     p.nslab = c->nslab;
     p.counters = c->counters;
     p.work = c->work + work_slot;
+    p.Bpre = c->Bpre;
+    p.cc = c->cc;
+    p.W = c->tc_W;
+    p.tmem_cols = c->tc_cols;
     return p;
 }
 
 km_status launch_assign(km_ctx *c, int mode, int work_slot)
 {
     km::AssignParams p = assign_params(c, work_slot);
-    KM_CUDA(km::launch_assign(mode, c->DP, c->csmem, p, c->grid_assign[mode], c->st));
+    if (mode == km::MODE_MTI_REDUCE && c->use_tc)
+        KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
+    else
+        KM_CUDA(km::launch_assign(mode, c->DP, c->csmem, p, c->grid_assign[mode], c->st));
     c->launches += 1;
     if (mode != km::MODE_DENSE) {
         KM_CUDA(km::launch_partials_reduce(c->acc_part, c->nslab,
@@ -340,6 +352,10 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     rec.ms_comm = c->world > 1 ? elapsed(ev[4], ev[5]) : 0.f;
     rec.ms_iter = elapsed(ev[0], ev[6]);
     c->stats.push_back(rec);
+    if (getenv("KM_DEBUG"))
+        fprintf(stderr, "[km] t=%d changed=%lld dists=%lld clause1=%lld refined=%lld steps=%lld tc_walk=%llu tc_uncovered=%llu tc_misfit=%llu ms=%.3f/%.3f/%.3f\n",
+                c->t, (long long)rec.changed, (long long)rec.dists, (long long)rec.clause1, (long long)rec.refined,
+                (long long)rec.walk_steps, h->local[5], h->local[6], h->local[7], rec.ms_iter, rec.ms_assign, rec.ms_sort);
     if (changed_out) *changed_out = rec.changed;
     if (dists_out) *dists_out = rec.dists;
     return KM_OK;
@@ -352,7 +368,7 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
+    cudaFree(c->NL); cudaFree(c->Bpre); cudaFree(c->cc); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
     cudaFree(c->counters_g); cudaFree(c->acc_part);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -451,6 +467,21 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     for (int m = 0; m < 4; ++m) {
         c->grid_assign[m] = km::assign_grid(m, DP, c->csmem, k, c->num_sms);
         c->part_grid = std::max(c->part_grid, c->grid_assign[m]);
+    }
+    c->use_tc = km::tc_supported(DP) && o->engine != KM_ENGINE_CUDA_CORE && c->prune == KM_PRUNE_MTI;
+    if (o->engine == KM_ENGINE_TENSOR && !km::tc_supported(DP))
+        return fail(KM_EARG, "tensor engine needs d padded to 8, 16 or 32 (d=%d)", d);
+    if (const char *e = getenv("KM_ENGINE")) {
+        if (!strcmp(e, "cuda")) c->use_tc = false;
+    }
+    if (c->use_tc) {
+        c->tc_W = std::min(256, std::max(16, (k + 15) & ~15));   // columns: A + NL[A] prefix
+        c->tc_cols = 32;
+        while (c->tc_cols < c->tc_W) c->tc_cols <<= 1;
+        KM_TRY(dalloc(&c->Bpre, (size_t)k * 3 * DP));
+        KM_TRY(dalloc(&c->cc, (size_t)k));
+        c->tc_grid = km::mti_tc_grid(DP, c->csmem, k, c->tc_W, c->tc_cols, c->num_sms);
+        c->part_grid = std::max(c->part_grid, c->tc_grid);
     }
     c->nslab = std::min(c->part_grid, c->num_sms);
     KM_TRY(dalloc(&c->acc_part, (size_t)c->nslab * k * (DP + 1)));

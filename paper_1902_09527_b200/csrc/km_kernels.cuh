@@ -49,6 +49,11 @@ struct AssignParams {
     int32_t nslab;         // CTA b accumulates into slab b % nslab
     unsigned long long *counters;  // [0] changed [1] dists [2] clause1 [3] refined [4] walk warp-steps
     int *work;             // dynamic chunk counter (zeroed before launch)
+    // tensor-core MTI path (k_mti_tc)
+    const float *Bpre;     // k x 3DP: [c_hi | c_hi | c_lo] TF32 split of fp32(C)
+    const float *cc;       // k: |fp32(C)|^2
+    int32_t W;             // candidate chunk width (MMA N max), multiple of 16, <= tmem_cols
+    int32_t tmem_cols;     // TMEM columns allocated per CTA (power of 2 >= 32)
 };
 
 struct PrepParams {
@@ -57,7 +62,9 @@ struct PrepParams {
     int32_t k, d, DP, sortN, ks;
     float *Cneg;           // k x DP
     float *f, *s;          // k
-    uint64_t *NL;          // k x k
+    uint64_t *NL;          // k x ks
+    float *Bpre;           // k x 3DP TF32 split rows (tensor-core path), may be null
+    float *cc;             // k: |fp32(C)|^2
     unsigned *eps_bits;    // fp32 bits of eps_C (atomicMax; zeroed before launch)
 };
 
@@ -82,6 +89,9 @@ int assign_grid(int mode, int DP, bool csmem, int k, int num_sms);
 size_t assign_smem(int DP, bool csmem, int k);
 cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems, double *acc,
                                   cudaStream_t st);
+bool tc_supported(int DP);
+cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st);
+int mti_tc_grid(int DP, bool csmem, int k, int W, int tmem_cols, int num_sms);
 cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, int d, int DP,
                           int *empty, cudaStream_t st);
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches);

@@ -37,7 +37,7 @@ class KMeans:
     def __init__(self, points, init_centroids, *, prune: str = "mti", device: Optional[int] = None,
                  stream=None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  n_global: int = 0, check_finite: bool = False, resort: str = "auto",
-                 resort_fraction: float = 0.10):
+                 resort_fraction: float = 0.10, engine: str = "auto"):
         L = C.lib()
         o = default_options()
         self._keep = []
@@ -77,6 +77,8 @@ class KMeans:
         o.resort_policy = {"auto": C.KM_RESORT_AUTO, "never": C.KM_RESORT_NEVER,
                            "always": C.KM_RESORT_ALWAYS}[resort]
         o.resort_fraction = resort_fraction
+        o.engine = {"auto": C.KM_ENGINE_AUTO, "cuda": C.KM_ENGINE_CUDA_CORE,
+                    "tensor": C.KM_ENGINE_TENSOR}[engine]
         h = ct.c_void_p()
         C.check(L.kmeans_create(n, d, C0.shape[0], ptr, C0.ctypes.data, ct.byref(o), ct.byref(h)))
         self._h = h

@@ -87,12 +87,12 @@ def test_B3_half_factor_on_gpu():
 
 
 # ---- seeded configs, free-running (strict tier) -------------------------------------------
-@pytest.mark.parametrize("prune", ["mti", "none"])
-def test_c1_free_running(prune):
+@pytest.mark.parametrize("prune,engine", [("mti", "auto"), ("mti", "cuda"), ("none", "auto")])
+def test_c1_free_running(prune, engine):
     X, idx, _ = make_config("c1")
     C0 = X[idx].astype(float)
     r = oracle.lloyd(X, C0, 100, 0, "mti")
-    g = gpu_run(X, C0, 100, prune)
+    g = gpu_run(X, C0, 100, prune, engine=engine)
     assert_strict(g, r)
     if prune == "mti":
         # distance counts vs oracle-mti: soft 0.1 % (fp32 vs fp64 bound rounding)
@@ -102,34 +102,36 @@ def test_c1_free_running(prune):
         assert np.all(np.abs(gc - r.clause1) <= 1e-3 * 10000 + 1)
 
 
-@pytest.mark.parametrize("prune", ["mti", "none"])
-def test_c2_free_running(prune):
+@pytest.mark.parametrize("prune,engine", [("mti", "auto"), ("mti", "cuda"), ("none", "auto")])
+def test_c2_free_running(prune, engine):
     X, idx, _ = make_config("c2")
     C0 = X[idx].astype(float)
     r = oracle.lloyd(X, C0, 50, 0, "mti")
-    g = gpu_run(X, C0, 50, prune)
+    g = gpu_run(X, C0, 50, prune, engine=engine)
     assert_strict(g, r)
     if prune == "mti":
         gd = np.array([s["dists"] for s in g["stats"]])
         assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
+@pytest.mark.parametrize("engine", ["auto", "cuda"])
 @pytest.mark.parametrize("name,n,iters", [("c3", 2_000_000, 30), ("c4", 1_000_000, 30)])
-def test_spectral_shaped_free_running(name, n, iters):
+def test_spectral_shaped_free_running(name, n, iters, engine):
     X, idx, _ = make_config(name, n=n)
     C0 = X[idx].astype(float)
     r = oracle.lloyd(X, C0, iters, 0, "mti")
-    g = gpu_run(X, C0, iters, "mti")
+    g = gpu_run(X, C0, iters, "mti", engine=engine)
     assert_strict(g, r)
     gd = np.array([s["dists"] for s in g["stats"]])
     assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
-def test_c5_shaped_large_k():
+@pytest.mark.parametrize("engine", ["auto", "cuda"])
+def test_c5_shaped_large_k(engine):
     X, idx, _ = make_config("c5", n=300_000)
     C0 = X[idx].astype(float)
     r = oracle.lloyd(X, C0, 8, 0, "mti")
-    g = gpu_run(X, C0, 8, "mti")
+    g = gpu_run(X, C0, 8, "mti", engine=engine)
     assert_strict(g, r)
     assert max(s["empty"] for s in g["stats"]) >= 0
 
