@@ -72,7 +72,7 @@ typedef struct km_options {
     int32_t check_finite;      /* 1 = scan points and centroids for NaN/Inf at create (KM_ENONFINITE) */
     int32_t points_on_host;    /* 1 = points pointer is host memory (pinned preferred); copied at create */
     int32_t resort_policy;     /* KM_RESORT_* */
-    float resort_fraction;     /* AUTO threshold, default 0.10 */
+    float resort_fraction;     /* AUTO threshold; 0 = default (0.10 CUDA-core engine, 0.5 tensor engine) */
     int32_t engine;            /* KM_ENGINE_* (default AUTO) */
     int32_t reserved[7];
 } km_options;
@@ -94,7 +94,7 @@ typedef struct km_iter_stats {
 
 typedef struct km_ctx km_ctx;
 
-/* Fill *opt with defaults: device 0, NULL stream, MTI, rank 0, world 1, AUTO re-sort at 0.10. */
+/* Fill *opt with defaults: device 0, NULL stream, MTI, rank 0, world 1, AUTO re-sort, AUTO engine. */
 void kmeans_default_options(km_options *opt);
 
 /* rank 0 only (world > 1): write a fresh ncclUniqueId (128 bytes) to out; the caller

@@ -468,12 +468,18 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         c->grid_assign[m] = km::assign_grid(m, DP, c->csmem, k, c->num_sms);
         c->part_grid = std::max(c->part_grid, c->grid_assign[m]);
     }
-    c->use_tc = km::tc_supported(DP) && o->engine != KM_ENGINE_CUDA_CORE && c->prune == KM_PRUNE_MTI;
+    // AUTO: tensor cores where the direct-form distance is expensive (d > 8); at d <= 8 the
+    // CUDA-core walk is faster (measured on C3)
+    c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI &&
+                (o->engine == KM_ENGINE_TENSOR || (o->engine == KM_ENGINE_AUTO && DP >= 16));
     if (o->engine == KM_ENGINE_TENSOR && !km::tc_supported(DP))
         return fail(KM_EARG, "tensor engine needs d padded to 8, 16 or 32 (d=%d)", d);
     if (const char *e = getenv("KM_ENGINE")) {
         if (!strcmp(e, "cuda")) c->use_tc = false;
     }
+    // the tensor-core kernel handles rows outside the tile's cluster without extra walks, so
+    // re-bucketing only pays when the layout is badly mixed
+    if (c->use_tc && !(o->resort_fraction > 0.f)) c->resort_fraction = 0.5f;
     if (c->use_tc) {
         c->tc_W = std::min(256, std::max(16, (k + 15) & ~15));   // columns: A + NL[A] prefix
         c->tc_cols = 32;
@@ -508,7 +514,7 @@ void kmeans_default_options(km_options *o)
     o->prune = KM_PRUNE_MTI;
     o->world = 1;
     o->resort_policy = KM_RESORT_AUTO;
-    o->resort_fraction = 0.10f;
+    o->resort_fraction = 0.f;      // auto
 }
 
 km_status kmeans_nccl_unique_id(uint8_t out[128])

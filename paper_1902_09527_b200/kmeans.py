@@ -37,7 +37,7 @@ class KMeans:
     def __init__(self, points, init_centroids, *, prune: str = "mti", device: Optional[int] = None,
                  stream=None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  n_global: int = 0, check_finite: bool = False, resort: str = "auto",
-                 resort_fraction: float = 0.10, engine: str = "auto"):
+                 resort_fraction: float = 0.0, engine: str = "auto"):
         L = C.lib()
         o = default_options()
         self._keep = []

@@ -47,7 +47,7 @@ def test_struct_layouts():
     assert ct.sizeof(_capi.KmIterStats) == 64
     o = _capi.KmOptions()
     _capi.lib().kmeans_default_options(ct.byref(o))
-    assert o.world == 1 and o.prune == 0 and abs(o.resort_fraction - 0.1) < 1e-7
+    assert o.world == 1 and o.prune == 0 and o.resort_fraction == 0.0 and o.engine == 0
 
 
 def test_create_argument_errors_without_gpu():
