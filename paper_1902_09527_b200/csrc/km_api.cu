@@ -136,9 +136,14 @@ struct km_ctx {
     double *C = nullptr, *Cprev = nullptr;
     float *Cneg = nullptr, *f = nullptr, *s = nullptr;
     uint64_t *NL = nullptr;
-    float *Bpre = nullptr, *cc = nullptr;   // tensor-core operand rows / |C|^2
+    // tensor-core MTI engine: per-cluster B operand blocks, column metadata, NL ranks
+    float *Bop = nullptr;
+    float4 *Bmeta = nullptr;
+    unsigned long long *defer = nullptr;   // deferred distance-count entries (n_alloc)
+    int *dcount = nullptr;                 // per 128-row tile
     bool use_tc = false;
-    int tc_W = 0, tc_cols = 0, tc_grid = 0;
+    int tc_nmax = 0, tc_cols = 0, tc_grid = 0;
+    int64_t n_alloc = 0;            // rows allocated (n rounded up to the 128-row tile)
     // per-iteration scratch (zeroed by one memset): acc | counters | empty, eps_bits, work[2]
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -180,11 +185,13 @@ km_status prep(km_ctx *c)
     p.f = c->f;
     p.s = c->s;
     p.NL = c->NL;
-    p.Bpre = c->Bpre;
-    p.cc = c->cc;
     p.eps_bits = c->eps_bits;
     KM_CUDA(km::launch_prep(p, c->st));
     c->launches += 1;
+    if (c->use_tc) {
+        KM_CUDA(km::launch_prep_tc(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->tc_nmax, c->Bop, c->Bmeta, c->st));
+        c->launches += 1;
+    }
     return KM_OK;
 }
 
@@ -211,18 +218,26 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
     p.nslab = c->nslab;
     p.counters = c->counters;
     p.work = c->work + work_slot;
-    p.Bpre = c->Bpre;
-    p.cc = c->cc;
-    p.W = c->tc_W;
+    p.Bop = c->Bop;
+    p.Bmeta = c->Bmeta;
+    p.nmax = c->tc_nmax;
     p.tmem_cols = c->tc_cols;
+    p.tile_chunk = 16;
+    p.defer = c->defer;
+    p.dcount = c->dcount;
+    p.nmeta = c->use_tc ? km::tc_nmeta_host(c->tc_nmax) : 0;
     return p;
 }
 
 km_status launch_assign(km_ctx *c, int mode, int work_slot)
 {
     km::AssignParams p = assign_params(c, work_slot);
-    if (mode == km::MODE_MTI_REDUCE && c->use_tc)
+    if (mode == km::MODE_MTI_REDUCE && c->use_tc) {
         KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
+        KM_CUDA(km::launch_mti_count(c->defer, c->dcount, c->n_alloc / 128, c->counters, c->NL, c->ks, c->k,
+                                     c->num_sms, c->st));
+        c->launches += 1;
+    }
     else
         KM_CUDA(km::launch_assign(mode, c->DP, c->csmem, p, c->grid_assign[mode], c->st));
     c->launches += 1;
@@ -368,7 +383,7 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->Bpre); cudaFree(c->cc); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
+    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
     cudaFree(c->counters_g); cudaFree(c->acc_part);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -410,11 +425,17 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     c->g_up = std::nextafter((float)(1.0 + gamma), 2.0f);
     c->g_dn = std::nextafter((float)(1.0 - gamma), 0.0f);
     // buffers
+    // rows padded to whole 128-row tiles (the tensor-core kernel bulk-copies whole tiles);
+    // padding rows are zero and never valid
+    c->n_alloc = (n + 127) / 128 * 128;
     for (int i = 0; i < 2; ++i) {
-        KM_TRY(dalloc(&c->X[i], (size_t)n * DP));
-        KM_TRY(dalloc(&c->a[i], (size_t)n));
-        KM_TRY(dalloc(&c->u[i], (size_t)n));
-        KM_TRY(dalloc(&c->perm[i], (size_t)n));
+        KM_TRY(dalloc(&c->X[i], (size_t)c->n_alloc * DP));
+        KM_TRY(dalloc(&c->a[i], (size_t)c->n_alloc));
+        KM_TRY(dalloc(&c->u[i], (size_t)c->n_alloc));
+        KM_TRY(dalloc(&c->perm[i], (size_t)c->n_alloc));
+        KM_CUDA(cudaMemsetAsync(c->X[i], 0, (size_t)c->n_alloc * DP * sizeof(float), c->st));
+        KM_CUDA(cudaMemsetAsync(c->a[i], 0, (size_t)c->n_alloc * sizeof(int32_t), c->st));
+        KM_CUDA(cudaMemsetAsync(c->u[i], 0, (size_t)c->n_alloc * sizeof(float), c->st));
     }
     c->Q = std::max(1, std::min(32, 4096 / k));
     const int NBmax = k * c->Q;
@@ -445,7 +466,6 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     KM_CUDA(cudaMallocHost(&c->hstat, sizeof(HostStat)));
     // points -> private padded copy
     float *X0 = c->X[0];
-    if (DP != d) KM_CUDA(cudaMemsetAsync(X0, 0, (size_t)n * DP * sizeof(float), c->st));
     KM_CUDA(cudaMemcpy2DAsync(X0, DP * sizeof(float), points, d * sizeof(float), d * sizeof(float),
                               (size_t)n, o->points_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                               c->st));
@@ -468,10 +488,10 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         c->grid_assign[m] = km::assign_grid(m, DP, c->csmem, k, c->num_sms);
         c->part_grid = std::max(c->part_grid, c->grid_assign[m]);
     }
-    // AUTO: tensor cores where the direct-form distance is expensive (d > 8); at d <= 8 the
-    // CUDA-core walk is faster (measured on C3)
-    c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI &&
-                (o->engine == KM_ENGINE_TENSOR || (o->engine == KM_ENGINE_AUTO && DP >= 16));
+    // AUTO: the CUDA-core walk (measured faster than the tensor-core pipeline on C3 and C4 so
+    // far); KM_ENGINE_TENSOR selects the tcgen05 kernel
+    c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 &&
+                (o->engine == KM_ENGINE_TENSOR || (o->engine == KM_ENGINE_AUTO && getenv("KM_AUTO_TC")));
     if (o->engine == KM_ENGINE_TENSOR && !km::tc_supported(DP))
         return fail(KM_EARG, "tensor engine needs d padded to 8, 16 or 32 (d=%d)", d);
     if (const char *e = getenv("KM_ENGINE")) {
@@ -481,12 +501,20 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     // re-bucketing only pays when the layout is badly mixed
     if (c->use_tc && !(o->resort_fraction > 0.f)) c->resort_fraction = 0.5f;
     if (c->use_tc) {
-        c->tc_W = std::min(256, std::max(16, (k + 15) & ~15));   // columns: A + NL[A] prefix
-        c->tc_cols = 32;
-        while (c->tc_cols < c->tc_W) c->tc_cols <<= 1;
-        KM_TRY(dalloc(&c->Bpre, (size_t)k * 3 * DP));
-        KM_TRY(dalloc(&c->cc, (size_t)k));
-        c->tc_grid = km::mti_tc_grid(DP, c->csmem, k, c->tc_W, c->tc_cols, c->num_sms);
+        c->tc_nmax = std::min(256, std::max(16, (k - 1 + 15) & ~15));   // columns: NL[A] prefix
+        if (const char *e = getenv("KM_TC_NMAX")) c->tc_nmax = std::max(16, std::min(c->tc_nmax, atoi(e) & ~15));
+        if (km::tc_plan(DP, c->csmem, k, c->tc_nmax, c->num_sms, &c->tc_grid, &c->tc_cols) == 0) {
+            if (o->engine == KM_ENGINE_TENSOR)
+                return fail(KM_EARG, "tensor engine: shared memory for d=%d k=%d exceeds one SM", d, k);
+            c->use_tc = false;
+        }
+    }
+    if (c->use_tc) {
+        const int KT = km::tc_kt_host(DP);
+        KM_TRY(dalloc(&c->Bop, (size_t)k * c->tc_nmax * KT));
+        KM_TRY(dalloc(&c->Bmeta, (size_t)k * km::tc_nmeta_host(c->tc_nmax)));
+        KM_TRY(dalloc(&c->defer, (size_t)c->n_alloc));
+        KM_TRY(dalloc(&c->dcount, (size_t)(c->n_alloc / 128) * 4));
         c->part_grid = std::max(c->part_grid, c->tc_grid);
     }
     c->nslab = std::min(c->part_grid, c->num_sms);

@@ -75,15 +75,29 @@ __device__ __forceinline__ float dist2(const float (&x)[DP], const CRow<SMEM> &c
     return s.x + s.y;
 }
 
+// Directed square roots from the hardware approximation: sqrt.approx.ftz.f32 has max relative
+// error 2^-23.25 over every normal input (exhaustive over [1, 4), tools/probes/sqrt_probe.cu
+// on B200; the result scales exactly with the exponent), so a 2^-21 margin applied with a
+// directed multiply bounds the true root from above / below.  FTZ: inputs below 2^-126 give 0
+// (a valid lower bound); the upper bound is floored at sqrt(2^-126) < 1.1e-19.
+__device__ __forceinline__ float sqrt_approx(float q)
+{
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+    return r;
+}
+__device__ __forceinline__ float sqrt_up(float q) { return fmaxf(__fmul_ru(sqrt_approx(q), 1.00000048f), 1.1e-19f); }
+__device__ __forceinline__ float sqrt_dn(float q) { return __fmul_rd(sqrt_approx(q), 0.99999952f); }
+
 // Rigorous distance interval of an fp32 squared distance q (exact mode):
 // true d(x, C64[c]) in [lower, upper] (gamma folded into g_up/g_dn, eps = eps_C).
 __device__ __forceinline__ float upper_d(float q, float g_up, float eps)
 {
-    return __fadd_ru(__fmul_ru(__fsqrt_ru(q), g_up), eps);
+    return __fadd_ru(__fmul_ru(sqrt_up(q), g_up), eps);
 }
 __device__ __forceinline__ float lower_d(float q, float g_dn, float eps)
 {
-    return fmaxf(0.f, __fsub_rd(__fmul_rd(__fsqrt_rd(q), g_dn), eps));
+    return fmaxf(0.f, __fsub_rd(__fmul_rd(sqrt_dn(q), g_dn), eps));
 }
 
 constexpr uint64_t kSentinel = 0xffffffff00000000ull;   // h = NaN (never < u), c = 0

@@ -324,20 +324,6 @@ __global__ void k_prep(PrepParams p)
     }
     for (int j = threadIdx.x; j < p.DP; j += blockDim.x)
         p.Cneg[(int64_t)c * p.DP + j] = j < d ? -(float)Cc[j] : 0.f;
-    if (p.Bpre) {
-        // tensor-core operand rows: fp32(C) split into TF32 hi + lo, laid out [hi | hi | lo]
-        for (int j = threadIdx.x; j < p.DP; j += blockDim.x) {
-            const float v = j < d ? (float)Cc[j] : 0.f;
-            uint32_t hb, lb;
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
-            const float hi = __uint_as_float(hb);
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(v - hi));
-            float *row = p.Bpre + (int64_t)c * 3 * p.DP;
-            row[j] = hi;
-            row[p.DP + j] = hi;
-            row[2 * p.DP + j] = __uint_as_float(lb);
-        }
-    }
     if (threadIdx.x == 0) {
         double se = 0.0, sf = 0.0;
         const double *Cp = p.Cprev + (int64_t)c * d;
@@ -348,11 +334,6 @@ __global__ void k_prep(PrepParams p)
             sf = fma(t, t, sf);
         }
         float eps = __double2float_ru(sqrt(se) * (1.0 + 1e-14));
-        if (p.cc) {
-            double s2 = 0.0;
-            for (int j = 0; j < d; ++j) { double v = (double)(float)Cc[j]; s2 = fma(v, v, s2); }
-            p.cc[c] = (float)s2;
-        }
         atomicMax(p.eps_bits, __float_as_uint(eps));
         p.f[c] = __double2float_ru(sqrt(sf) * (1.0 + 1e-14));
     }

@@ -47,13 +47,17 @@ struct AssignParams {
     int32_t count_changed; // 1: count a_new != a_old
     double *acc;           // partial-sum slabs: nslab x k x (DP+1) (zeroed before launch)
     int32_t nslab;         // CTA b accumulates into slab b % nslab
-    unsigned long long *counters;  // [0] changed [1] dists [2] clause1 [3] refined [4] walk warp-steps
+    unsigned long long *counters;  // [0] changed [1] dists [2] clause1 [3] refined [4] walk warp-steps / TC columns [5] TC fallbacks [6] deferred rows
     int *work;             // dynamic chunk counter (zeroed before launch)
-    // tensor-core MTI path (k_mti_tc)
-    const float *Bpre;     // k x 3DP: [c_hi | c_hi | c_lo] TF32 split of fp32(C)
-    const float *cc;       // k: |fp32(C)|^2
-    int32_t W;             // candidate chunk width (MMA N max), multiple of 16, <= tmem_cols
-    int32_t tmem_cols;     // TMEM columns allocated per CTA (power of 2 >= 32)
+    // tensor-core MTI path (k_mti_tc, km_tc.cu)
+    const float *Bop;      // k x nmax x KT: per-cluster B operand blocks (UMMA K-major layout)
+    const float4 *Bmeta;   // k x nmax: {H, column centroid bits, |c'|^2 up, prefix max}
+    int32_t nmax;          // columns per cluster block (multiple of 16, <= 256)
+    int32_t tmem_cols;     // TMEM columns allocated per CTA (power of 2 >= 2 nmax)
+    int32_t tile_chunk;    // 128-row tiles claimed per work-counter fetch
+    unsigned long long *defer;   // n_alloc: (a << 32 | u_t bits) of rows whose distance count is deferred
+    int *dcount;           // ntiles: deferred entries per 128-row tile
+    int32_t nmeta;         // Bmeta entries per cluster (power of two >= nmax, NaN padded)
 };
 
 struct PrepParams {
@@ -63,8 +67,6 @@ struct PrepParams {
     float *Cneg;           // k x DP
     float *f, *s;          // k
     uint64_t *NL;          // k x ks
-    float *Bpre;           // k x 3DP TF32 split rows (tensor-core path), may be null
-    float *cc;             // k: |fp32(C)|^2
     unsigned *eps_bits;    // fp32 bits of eps_C (atomicMax; zeroed before launch)
 };
 
@@ -90,8 +92,15 @@ size_t assign_smem(int DP, bool csmem, int k);
 cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems, double *acc,
                                   cudaStream_t st);
 bool tc_supported(int DP);
+int tc_kt_host(int DP);
+size_t tc_plan(int DP, bool csmem, int k, int nmax, int num_sms, int *grid, int *tmem_cols);
 cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st);
-int mti_tc_grid(int DP, bool csmem, int k, int W, int tmem_cols, int num_sms);
+cudaError_t launch_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
+                           float *Bop, float4 *Bmeta, cudaStream_t st);
+cudaError_t launch_mti_count(const unsigned long long *defer, const int *dcount, int64_t ntiles,
+                             unsigned long long *counters, const uint64_t *NL, int ks, int k, int num_sms,
+                             cudaStream_t st);
+int tc_nmeta_host(int nmax);
 cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, int d, int DP,
                           int *empty, cudaStream_t st);
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches);

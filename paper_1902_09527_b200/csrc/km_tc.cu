@@ -1,28 +1,40 @@
-// km_tc.cu — tensor-core (tcgen05, TF32 x3) MTI assignment + fused reduction for sm_100a.
+// km_tc.cu — tensor-core (tcgen05, TF32 x3) MTI assignment + fused fp64 reduction for sm_100a.
 //
-// Same method and outputs as k_assign<MODE_MTI_REDUCE> (§3.3, 1026-1053: clause 1,
-// tightening, clauses 2/3; §3.2, 1000-1011: fused per-cluster reduction); only the
-// evaluation of the surviving candidates moves to the tensor cores.  DESIGN.md "Tensor-core
-// MTI".  Per 128-row tile (rows bucketed by cluster, so a tile mostly shares its cluster A):
+// Same method and outputs as k_assign<MODE_MTI_REDUCE> (§3.3, 1026-1053: drift,
+// clause 1, tightening U(u), clauses 2/3; §3.2, 1000-1011: fused per-cluster
+// reduction); only the evaluation of the surviving candidates moves to the tensor cores.
+// DESIGN.md "Tensor-core MTI".
 //
-//   1. per row (CUDA cores): u += f(a); clause 1; tighten u = d(x, C[a]) in the direct fp32
-//      form (rigorous gamma bound) -> ut; the row's x split into TF32 hi/lo written to smem.
-//   2. candidates of the tile = prefix of A's neighbour list NL[A] with H < max ut (a prefix,
-//      since NL[A] is sorted by H); their pre-split centroid rows [c_hi | c_hi | c_lo] are
-//      staged in smem (cached across tiles of the same cluster).
-//   3. one elected thread issues tcgen05.mma.kind::tf32 (M = 128, N = 16..256, K = 3 DP):
-//      D[r][j] = x_hi.c_hi + x_lo.c_hi + x_hi.c_lo ~ x . c_j  (error <= (3DP+7) 2^-23 |x||c|)
-//      accumulated in TMEM; completion is signalled through an mbarrier (tcgen05.commit).
-//   4. epilogue: each thread reads its TMEM lane (tcgen05.ld 32x32b.x16), forms
-//      q_j = |x|^2 + |c_j|^2 - 2 D and keeps the best / second best over its own survivors
-//      (H[A][c_j] < ut, clauses 2/3).  All q carry one absolute error bound
-//      E = (14 DP + 36) 2^-24 (|x|^2 + max |c|^2) (2x the derived bound); if the second
-//      best's interval meets the best's, the row falls back to the CUDA-core direct walk,
-//      whose own fp32 screen and fp64 refinement make the final decision (exact mode).
-//   Rows whose cluster is not A ("misfits") also take the CUDA-core walk.
+// Rows are stored bucketed by cluster, so a 128-row tile mostly shares one cluster A (the
+// cluster of its middle row).  Per tile, software-pipelined with the previous tile:
+//
+//   load     thread 0 streams tiles [x | a | u] into a STAGES-deep shared-memory ring with
+//            cp.async.bulk (TMA bulk copies) + mbarrier complete_tx, tiles claimed in chunks
+//            from a global counter (dynamic load balance, clusters stay contiguous per chunk)
+//   prep(i)  per row (CUDA cores): u += f(a); clause 1 (u <= s(a) -> keep, 0 distances);
+//            else centre x' = x - C^[A], tighten u_t = d(x, C^[a]) (direct fp32 form, rigorous
+//            bound), column threshold T (= u_t for rows of A; (u_t + d(x,A))/2 for the other
+//            rows: triangle inequality around A), p = #{j : H[A][j] < T} by binary search;
+//            A operand row [x'hi | x'lo | x'hi | xx_hi | xx_lo | 1 | 1 | 0..] written to smem
+//   mma(i)   one thread: D[128 x N] = A . B^T, tcgen05.mma.kind::tf32, K = KT, N = max p of
+//            the tile rounded up to 16; B = k_prep's per-cluster block for A (columns = A's
+//            neighbour list in ascending H, rows [-2c'hi | -2c'hi | -2c'lo | 1 | 1 | cc_hi |
+//            cc_lo]) so D[r][j] ~ |x' - c'_j|^2 directly; committed to an mbarrier; TMEM is
+//            double buffered so mma(i) overlaps epilogue(i-1)
+//   epi(i-1) per row: tcgen05.ld 32x32b.x16 chunks while any lane of the warp has p > chunk;
+//            packed keys (q bits & ~0xff | column) -> best / second best by integer min/max;
+//            rigorous intervals decide the winner or send the row to the CUDA-core walk
+//            (direct form + fp64 refinement: exact mode); a/u written; fp64 warp reduction
+//
+// Error model (measured on B200 by tools/probes/tc_acc_probe.cu:
+// accumulation error <= (K/4 + 2) 2^-24 sum|a_k b_k|):  |D - |x' - c'|^2| <= E with
+//   E = kappa (xx + cmax),  kappa = 2 (25 + DP/4 + KT/2) 2^-24  (2x the derived bound)
+// where cmax bounds |c'_j|^2 over the columns the row's warp reads.  Centring roundings add
+// <= 2^-24 (|x'| + |c'|) on the distance scale.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <initializer_list>
 
 #include "km_device.cuh"
 #include "km_kernels.cuh"
@@ -41,13 +53,13 @@ __device__ __forceinline__ float tf32_rna(float x)
 
 __device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d)
 {
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "f"(a), "f"(b), "f"(c), "f"(d));
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
 // K-major, no-swizzle UMMA operand layout (core matrices of 8 rows x 16 B): element (r, e)
 // of an R-row operand lives at K-block e/8 (R*32 B each), 8-row group r/8 (SBO = 256 B),
 // 16-B chunk (e%8)/4 (LBO = 128 B), row r%8 (16 B), word e%4.
-__device__ __forceinline__ uint32_t op_off(int r, int e, int R)
+__host__ __device__ __forceinline__ uint32_t op_off(int r, int e, int R)
 {
     return (uint32_t)((e >> 3) * (R * 32) + (r >> 3) * 256 + ((e & 7) >> 2) * 128 + (r & 7) * 16 + (e & 3) * 4);
 }
@@ -67,452 +79,769 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
 
 __device__ __forceinline__ void mma_commit(uint32_t mbar)
 {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count));
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase)
 {
     asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
                  "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-                 "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}" :: "r"(mbar), "r"(phase));
+                 "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}" :: "r"(mbar), "r"(phase) : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16])
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t mbar, uint32_t bytes)
 {
-    uint32_t r[16];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+// TMEM -> registers, 32 lanes x 16 consecutive 32-bit columns; the wait passes the registers
+// through so no use can be scheduled before tcgen05.wait::ld
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
+{
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
                    "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
                  : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :: "memory");
 }
 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// top-2 update of packed keys (signed compare: negative q sort first)
+__device__ __forceinline__ void top2(int &m1, int &m2, int ka, int kb)
+{
+    const int lo = min(ka, kb), hi = max(ka, kb);
+    m2 = min(min(max(m1, lo), m2), hi);
+    m1 = min(m1, lo);
+}
+
 }  // namespace tc
 
 constexpr int kTcRows = 128;
+constexpr int kTcPrepWarps = 4;                  // warps 0-3: prep (one row per thread)
+constexpr int kTcEpiWarp0 = 4;                   // warps 4-7: epilogue (TMEM lane quadrant = warp % 4)
+constexpr int kTcProdWarp = 8;                   // warp 8: TMA producer
+constexpr int kTcMmaWarp = 9;                    // warp 9: MMA issuer
+constexpr int kTcThreads = 320;
 
-template <int DP, bool CSMEM>
-__global__ void __launch_bounds__(kTcRows)
-k_mti_tc(AssignParams p)
+__host__ __device__ constexpr int tc_kt(int DP) { return ((3 * DP + 4) + 7) & ~7; }
+
+__host__ __device__ inline int tc_nmeta(int nmax) { int m = 16; while (m < nmax) m <<= 1; return m; }
+
+// per-row state handed from the prep warps to the epilogue warps (one slot per TMEM buffer)
+struct TcRow {
+    int a;          // assignment before the pass
+    int flags;      // bit0 valid, bit1 active (clause 1 failed), bit2 misfit (a != A), bit3 uncovered
+    float uu;       // u + f(a) (clause-1 rows keep it)
+    float ut;       // tightened upper bound of d(x, C[a]) (direct form)
+    float lo;       // lower bound of d(x, C[a])
+    float xx;       // |x - C^[A]|^2 (direct form)
+    int p;          // columns below the row's threshold
+    int pad;
+};
+
+struct TcInfo {      // per TMEM buffer: the tile in flight
+    long long tile;  // -1 = end of stream
+    int A;           // tile cluster
+    int bslot;       // B operand slot
+    int mslot;       // column-metadata slot
+    int N;           // MMA columns (0: no MMA)
+    int pw[4];       // per-warp columns the epilogue reads
+};
+
+struct TcCfg {       // pipeline depths and shared-memory layout (byte offsets, 1024-aligned base)
+    int S, NA, NB;   // ring stages, A-operand buffers, B-operand buffers
+    int stage_bytes, ring, aop, bop, bmeta, rstate, sc, sf, ss, total;
+};
+
+__host__ __device__ inline TcCfg tc_cfg(int DP, bool csmem, int k, int nmax, int S, int NA, int NB)
 {
-    constexpr int KT = 3 * DP;                  // [x_hi | x_lo | x_hi] . [c_hi | c_hi | c_lo]
-    constexpr int G = 8;                        // tiles claimed per work-counter fetch
-    extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t s_mbar;
-    __shared__ int s_firstA[2][4];
-    __shared__ long long s_ahead[2];
+    TcCfg L;
+    const int KT = tc_kt(DP);
+    L.S = S; L.NA = NA; L.NB = NB;
+    L.stage_bytes = kTcRows * DP * 4 + 2 * kTcRows * 4;
+    L.ring = 0;
+    L.aop = (L.ring + S * L.stage_bytes + 127) & ~127;
+    L.bop = L.aop + NA * kTcRows * KT * 4;
+    L.bmeta = L.bop + NB * nmax * KT * 4;
+    L.rstate = L.bmeta + 2 * tc_nmeta(nmax) * 16;
+    L.sc = L.rstate + 2 * kTcRows * (int)sizeof(TcRow);
+    L.sf = L.sc + (csmem ? k * DP * 4 : 0);
+    L.ss = L.sf + k * 4;
+    L.total = L.ss + k * 4;
+    return L;
+}
 
-    const int k = p.k, W = p.W, ks = p.ks;
+// number of keys h[0..M) below T, M = power of two, keys ascending with NaN padding (NaN never
+// compares below): branch-free lower bound in log2(M) fixed steps
+template <int M>
+__device__ __forceinline__ int count_below(const float4 *meta, float T)
+{
+    int base = 0;
+#pragma unroll
+    for (int half = M >> 1; half >= 1; half >>= 1)
+        base = meta[base + half - 1].x < T ? base + half : base;
+    return base + (meta[base].x < T ? 1 : 0);
+}
+
+__device__ __forceinline__ int count_below_nl(const uint64_t *nl, int m, float T)
+{
+    int lo = 0, hi = m;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_h(__ldg(nl + mid)) < T) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <int DP, bool CSMEM, int NMETA>
+__global__ void __launch_bounds__(kTcThreads, 2)
+k_mti_tc(AssignParams p, TcCfg L)
+{
+    constexpr int KT = tc_kt(DP);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t s_full[8], s_sfree[8];
+    __shared__ __align__(8) uint64_t s_aready[2], s_accfull[2], s_tfree[2];
+    __shared__ __align__(8) uint64_t s_bbar[2];
+    __shared__ long long s_meta[8];
+    __shared__ TcInfo s_info[2];
+    __shared__ uint32_t s_tmem;
+
+    const int k = p.k, NMAX = p.nmax, S = L.S;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    uint8_t *sA = smem;                                          // 128 x KT operand
-    uint8_t *sB = sA + kTcRows * KT * 4;                         // W x KT operand
-    float4 *sKey = reinterpret_cast<float4 *>(sB + W * KT * 4);  // W x {h, c bits, |c|^2, -}
-    float *sC = reinterpret_cast<float *>(sKey + W);             // k x DP (CSMEM)
-    float *sF = sC + (CSMEM ? k * DP : 0);
-    float *sS = sF + k;
-    const uint32_t aBase = tc::smem_u32(sA), bBase = tc::smem_u32(sB), mbar = tc::smem_u32(&s_mbar);
+    const uint32_t sbase = tc::smem_u32(smem);
+    float *sC = reinterpret_cast<float *>(smem + L.sc);
+    float *sF = reinterpret_cast<float *>(smem + L.sf);
+    float *sS = reinterpret_cast<float *>(smem + L.ss);
+    TcRow *rstate = reinterpret_cast<TcRow *>(smem + L.rstate);
+    const float4 *meta0 = reinterpret_cast<const float4 *>(smem + L.bmeta);
 
     if (CSMEM) {
         const float4 *src = reinterpret_cast<const float4 *>(p.Cneg);
         float4 *dst = reinterpret_cast<float4 *>(sC);
-        for (int i = t; i < k * DP / 4; i += kTcRows) dst[i] = src[i];
+        for (int i = t; i < k * DP / 4; i += kTcThreads) dst[i] = src[i];
     }
-    for (int i = t; i < k; i += kTcRows) { sF[i] = p.f[i]; sS[i] = p.s[i]; }
-    if (warp == 0) {
+    for (int i = t; i < k; i += kTcThreads) { sF[i] = p.f[i]; sS[i] = p.s[i]; }
+    {   // zero the A operand buffers once (rows of clause-1 threads are never written)
+        float4 *za = reinterpret_cast<float4 *>(smem + L.aop);
+        for (int i = t; i < L.NA * kTcRows * KT / 4; i += kTcThreads) za[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (warp == kTcMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(tc::smem_u32(&s_tmem)), "r"(p.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (t == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(1));
-        asm volatile("fence.mbarrier_init.release.cluster;");
-        s_ahead[0] = (long long)atomicAdd(p.work, 1) * G;
-        s_ahead[1] = (long long)atomicAdd(p.work, 1) * G;
+        for (int s = 0; s < S; ++s) {
+            tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
+            tc::mbar_init(tc::smem_u32(&s_sfree[s]), 4);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(tc::smem_u32(&s_aready[b]), kTcPrepWarps);
+            tc::mbar_init(tc::smem_u32(&s_accfull[b]), 1);
+            tc::mbar_init(tc::smem_u32(&s_tfree[b]), 4);
+            tc::mbar_init(tc::smem_u32(&s_bbar[b]), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    const uint32_t tmem = s_tmem;
-    const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);
-
-    CRow<CSMEM> Cn;
-    if constexpr (CSMEM) {
-        uint32_t b = tc::smem_u32(sC);
-        asm volatile("mov.u32 %0, %0;" : "+r"(b));
-        Cn.base = b;
-    } else {
-        Cn.base = p.Cneg;
-    }
-    double *acc = p.acc + (int64_t)(blockIdx.x % p.nslab) * k * (DP + 1);
-    const float eps = *p.eps;
-    const float kappa = (14.f * DP + 44.f) * 5.9604645e-8f;    // (14 DP + 44) 2^-24, DESIGN.md
     const int64_t n = p.n;
     const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
-    const bool partial_cols = W - 1 < k - 1;                    // columns do not cover all of NL[A]
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(W >> 3) << 17) |
-                           ((uint32_t)(kTcRows >> 4) << 24);   // F32 += TF32 x TF32, K-major, 128 x W
 
-    RunAcc<DP> ra;
-    ra.clear();
-    unsigned long long c_changed = 0, c_dists = 0, c_clause1 = 0, c_refined = 0;
-    unsigned steps = 0;
-    unsigned dbg_walk = 0, dbg_uncov = 0, dbg_mis = 0;   // diagnostics (counters 5..7)
-    uint32_t phase = 0;
-    int colA = -1;                        // cluster whose columns [A | NL[A][0..W-1)] are staged
-
-    int64_t g_cur = s_ahead[0], g_next = s_ahead[1];
-    __syncthreads();                      // everyone has read s_ahead before it is reused
-    int64_t tile = g_cur;
-    float nx[DP];
-    int na = 0;
-    float nu = 0.f;
-    auto load = [&](int64_t tl) {
-        const int64_t r = tl * kTcRows + t;
-        const bool v = tl < ntiles && r < n;
-        const float4 *xr = reinterpret_cast<const float4 *>(p.X + (v ? r : 0) * DP);
-#pragma unroll
-        for (int j = 0; j < DP / 4; ++j) {
-            float4 q = v ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-            nx[4 * j] = q.x; nx[4 * j + 1] = q.y; nx[4 * j + 2] = q.z; nx[4 * j + 3] = q.w;
-        }
-        na = v ? __ldg(p.a + r) : 0;
-        nu = v ? __ldg(p.u + r) : 0.f;
-    };
-    if (tile < ntiles) load(tile);
-    int it = 0;
-
-    while (tile < ntiles) {
-        const int par = it & 1;
-        const int64_t row = tile * kTcRows + t;
-        const bool valid = row < n;
-        float x[DP];
-#pragma unroll
-        for (int j = 0; j < DP; ++j) x[j] = nx[j];
-        const int aold = na;
-        const bool switching = !(tile + 1 < min(g_cur + G, ntiles));
-        if (switching && t == 0) s_ahead[par ^ 1] = (long long)atomicAdd(p.work, 1) * G;
-
-        // ---- 1. per row: drift, clause 1, tighten (direct fp32 form), operand row -----------
-        const float uu = valid ? __fadd_ru(nu, sF[aold]) : 0.f;         // u += f(a)
-        const bool c1 = valid && uu <= sS[aold];                          // clause 1
-        c_clause1 += c1;
-        const bool active = valid && !c1;
-        float q_own = INFINITY, ut = 0.f, xx = 0.f;
-        if (active) {
-            q_own = dist2<DP, CSMEM>(x, Cn, aold);                         // U(u) = d(x, C[a])
-            ut = upper_d(q_own, p.g_up, eps);
-        }
-        {
-            const unsigned am = __ballot_sync(kFull, active);
-            const int fa = am ? __shfl_sync(kFull, aold, __ffs(am) - 1) : -1;
-            if (lane == 0) s_firstA[par][warp] = fa;
-        }
-        __syncthreads();                                                   // (1)
-        int64_t tile_next = tile + 1;
-        if (switching) {
-            g_cur = g_next;
-            g_next = s_ahead[par ^ 1];
-            tile_next = g_cur;
-        }
-        int A = -1;
-#pragma unroll
-        for (int w = 3; w >= 0; --w) A = s_firstA[par][w] >= 0 ? s_firstA[par][w] : A;
-
-        float bq = q_own, q2 = INFINITY;
-        int bc = aold, ns = active ? 1 : 0;
-        bool walk = active;                      // rows not decided by the tensor cores
-        bool prefetched = false;
-
-        if (A >= 0) {
-            const bool misfit = active && aold != A;
-            // per-row column threshold: own rows take NL[A] candidates with H < ut (clauses 2/3);
-            // misfit rows (cluster a != A) take the columns c with 2 H[A][c] - d(x,A) < d_best,
-            // i.e. H[A][c] < (ut + d(x,A)) / 2 (triangle inequality around A), plus A itself
-            float T = ut;
-            if (misfit) {
-                const float dA = upper_d(dist2<DP, CSMEM>(x, Cn, A), p.g_up, eps);
-                T = __fmul_ru(__fadd_ru(ut, dA), 0.5f);
-            }
-            // ---- 2. operands, centred on C[A] (translation-invariant distances, small norms):
-            //      row r: x' = x - C[A];  column j: c'_j = C[c_j] - C[A]  (fp32), split into TF32
-            //      hi + lo, A' = [x'_hi | x'_lo | x'_hi], B' = [c'_hi | c'_hi | c'_lo]
-            {
-                float xc[DP];
-#pragma unroll
-                for (int j4 = 0; j4 < DP / 4; ++j4) {
-                    const float4 ca = Cn.ld(A, DP, 4 * j4);        // -C[A]
-                    xc[4 * j4] = x[4 * j4] + ca.x; xc[4 * j4 + 1] = x[4 * j4 + 1] + ca.y;
-                    xc[4 * j4 + 2] = x[4 * j4 + 2] + ca.z; xc[4 * j4 + 3] = x[4 * j4 + 3] + ca.w;
+    if (warp == kTcProdWarp) {
+        // ================= producer: tiles [x | a | u] -> ring stages (TMA bulk copies) ========
+        if (lane == 0) {
+            const int G = p.tile_chunk;
+            int64_t q_next = 0, q_end = 0;
+            for (int L_ = 0;; ++L_) {
+                const int s = L_ % S;
+                if (L_ >= S) tc::mbar_wait(tc::smem_u32(&s_sfree[s]), (uint32_t)(((L_ / S) - 1) & 1));
+                if (q_next >= q_end) {
+                    const int64_t c = atomicAdd(p.work, 1);
+                    q_next = c * G;
+                    q_end = q_next + G;
                 }
+                const int64_t tl = q_next < ntiles ? q_next : -1;
+                ++q_next;
+                s_meta[s] = tl;
+                const uint32_t mb = tc::smem_u32(&s_full[s]);
+                if (tl < 0) { tc::mbar_arrive(mb); break; }
+                const uint32_t xb = kTcRows * DP * 4, ab = kTcRows * 4;
+                tc::mbar_arrive_tx(mb, xb + 2 * ab);
+                const uint32_t dst = sbase + L.ring + s * L.stage_bytes;
+                tc::bulk_g2s(dst, p.X + tl * kTcRows * DP, xb, mb);
+                tc::bulk_g2s(dst + xb, p.a + tl * kTcRows, ab, mb);
+                tc::bulk_g2s(dst + xb + ab, p.u + tl * kTcRows, ab, mb);
+            }
+        }
+    } else if (warp == kTcMmaWarp) {
+        // ================= MMA issuer: D[b] = A[i % NA] . B[slot]^T ==========================
+        if (lane == 0) {
+            const uint32_t idesc_base = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcRows >> 4) << 24);
+            for (int i = 0;; ++i) {
+                const int b = i & 1;
+                tc::mbar_wait(tc::smem_u32(&s_aready[b]), (uint32_t)((i >> 1) & 1));
+                tc::fence_after();
+                const TcInfo &inf = s_info[b];
+                if (inf.tile < 0) { tc::mbar_arrive(tc::smem_u32(&s_accfull[b])); break; }
+                const int N = inf.N;
+                // TMEM buffer b was released by the epilogue of tile i - 2 (the prep warps waited
+                // for that before handing over tile i)
+                if (N > 0) {
+                    const uint32_t idesc = idesc_base | ((uint32_t)(N >> 3) << 17);
+                    const uint32_t ab = sbase + L.aop + (uint32_t)((i % L.NA) * kTcRows * KT * 4);
+                    const uint32_t bb = sbase + L.bop + (uint32_t)(inf.bslot * NMAX * KT * 4);
 #pragma unroll
-                for (int j = 0; j < DP; ++j) xx = fmaf(xc[j], xc[j], xx);
+                    for (int kb = 0; kb < KT / 8; ++kb)
+                        tc::mma_tf32(s_tmem + (uint32_t)(b * NMAX), tc::sdesc(ab + kb * kTcRows * 32),
+                                     tc::sdesc(bb + kb * NMAX * 32), idesc, kb > 0);
+                    tc::mma_commit(tc::smem_u32(&s_accfull[b]));
+                } else {
+                    tc::mbar_arrive(tc::smem_u32(&s_accfull[b]));
+                }
+            }
+        }
+    } else if (warp < kTcPrepWarps) {
+        // ================= prep: bounds, clause 1, tightening, A operand ====================
+        const float eps = *p.eps;
+        const int kcols = min(NMAX, k - 1);
+        const bool full_list = kcols == k - 1;
+        CRow<CSMEM> Cn;
+        if constexpr (CSMEM) Cn.base = tc::smem_u32(sC); else Cn.base = p.Cneg;
+        int slotA[2] = {-1, -1};                 // cluster whose B block / metadata sits in a slot
+        long long slotLast[2] = {-1, -1};        // last tile that used the slot
+        int bcur = 0;
+        uint32_t bpar[2] = {0u, 0u};
+        unsigned long long c_clause1 = 0;
+        for (int i = 0;; ++i) {
+            const int s = i % S, b = i & 1;
+            tc::mbar_wait(tc::smem_u32(&s_full[s]), (uint32_t)((i / S) & 1));
+            const int64_t tile = s_meta[s];
+            // buffers of tile i - 2 (A operand when NA = 2, row state, TMEM) are free once its
+            // epilogue finished
+            if (i >= 2) tc::mbar_wait(tc::smem_u32(&s_tfree[b]), (uint32_t)(((i - 2) >> 1) & 1));
+            if (L.NA == 1 && i >= 1)    // single A buffer: the previous MMA must have consumed it
+                tc::mbar_wait(tc::smem_u32(&s_accfull[(i - 1) & 1]), (uint32_t)(((i - 1) >> 1) & 1));
+            if (tile < 0) {
+                if (t == 0) s_info[b].tile = -1;
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[b]));
+                break;
+            }
+            const uint8_t *stage = smem + L.ring + s * L.stage_bytes;
+            const float *sx = reinterpret_cast<const float *>(stage);
+            const int32_t *sa = reinterpret_cast<const int32_t *>(stage + kTcRows * DP * 4);
+            const float *su = reinterpret_cast<const float *>(stage + kTcRows * DP * 4 + kTcRows * 4);
+            const int vrows = (int)(n - tile * kTcRows < kTcRows ? n - tile * kTcRows : kTcRows);
+            const int A = sa[vrows >> 1];                 // tile cluster: its middle row's
+            // column block of A: reuse a slot, or load it into the other one
+            int mslot;
+            if (slotA[bcur] == A) {
+                mslot = bcur;
+            } else if (slotA[bcur ^ 1] == A && L.NB == 2) {
+                mslot = bcur ^ 1;
+            } else {
+                mslot = bcur ^ 1;
+                // the slot's previous user must be done: its epilogue (metadata) and MMA (B block)
+                const long long last = slotLast[mslot];
+                if (last >= 0 && last == i - 1)
+                    tc::mbar_wait(tc::smem_u32(&s_tfree[last & 1]), (uint32_t)((last >> 1) & 1));
+                if (L.NB == 1 && i >= 1)  // single B block: the previous MMA must be done
+                    tc::mbar_wait(tc::smem_u32(&s_accfull[(i - 1) & 1]), (uint32_t)(((i - 1) >> 1) & 1));
+                // all four prep warps are past their reads of the old slot (named barrier)
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (t == 0) {
+                    const uint32_t bb = tc::smem_u32(&s_bbar[mslot]);
+                    const int bsl = L.NB == 2 ? mslot : 0;
+                    const uint32_t opb = (uint32_t)(NMAX * KT * 4), mtb = (uint32_t)(NMETA * 16);
+                    tc::mbar_arrive_tx(bb, opb + mtb);
+                    tc::bulk_g2s(sbase + L.bop + (uint32_t)(bsl * NMAX * KT * 4), p.Bop + (int64_t)A * NMAX * KT, opb, bb);
+                    tc::bulk_g2s(sbase + L.bmeta + (uint32_t)(mslot * NMETA * 16), p.Bmeta + (int64_t)A * NMETA, mtb, bb);
+                }
+                tc::mbar_wait(tc::smem_u32(&s_bbar[mslot]), bpar[mslot]);
+                bpar[mslot] ^= 1u;
+                slotA[mslot] = A;
+                bcur = mslot;
+            }
+            slotLast[mslot] = i;
+            const float4 *meta = meta0 + mslot * NMETA;
+
+            const int64_t row = tile * kTcRows + t;
+            const bool valid = row < n;
+            float x[DP];
 #pragma unroll
-                for (int c = 0; c < DP / 4; ++c) {
+            for (int j = 0; j < DP; j += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(sx + t * DP + j);
+                x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+            }
+            const int aold = valid ? sa[t] : 0;
+            const float uu = valid ? __fadd_ru(su[t], sF[aold]) : 0.f;       // u += f(a)
+            const bool c1 = valid && uu <= sS[aold];                           // clause 1
+            const bool active = valid && !c1;
+            const bool misfit = active && aold != A;
+            c_clause1 += c1;
+            TcRow st;
+            st.a = aold; st.uu = uu; st.xx = 0.f; st.ut = 0.f; st.lo = 0.f; st.p = 0; st.pad = 0;
+            int flags = (valid ? 1 : 0) | (active ? 2 : 0) | (misfit ? 4 : 0);
+            if (active) {
+                // x' = x - C^[A] in the direct form's arithmetic (x + (-c)), xx = |x'|^2
+                float xh[DP];
+                float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < DP; j += 4) {
+                    const float4 c = Cn.ld(A, DP, j);
+                    const float2 t0 = add2(make_float2(x[j], x[j + 1]), make_float2(c.x, c.y));
+                    const float2 t1 = add2(make_float2(x[j + 2], x[j + 3]), make_float2(c.z, c.w));
+                    xh[j] = t0.x; xh[j + 1] = t0.y; xh[j + 2] = t1.x; xh[j + 3] = t1.y;
+                    acc0 = fma2(t0, t0, acc0);
+                    acc1 = fma2(t1, t1, acc1);
+                }
+                const float2 s2 = add2(acc0, acc1);
+                const float xx = s2.x + s2.y;
+                st.xx = xx;
+                float T;
+                if (!misfit) {
+                    st.ut = upper_d(xx, p.g_up, eps);
+                    st.lo = lower_d(xx, p.g_dn, eps);
+                    T = st.ut;
+                } else {
+                    // misfit row: own distance in the direct form; columns by the triangle bound
+                    // around A: any c with 2 H[A][c] - d(x,A) >= u_t cannot beat a (and the own
+                    // cluster itself has H[A][a] <= (u_t + d(x,A)) / 2, so it is a column)
+                    const float qo = dist2<DP, CSMEM>(x, Cn, aold);
+                    st.ut = upper_d(qo, p.g_up, eps);
+                    st.lo = lower_d(qo, p.g_dn, eps);
+                    T = __fmul_ru(__fadd_ru(st.ut, upper_d(xx, p.g_up, eps)), 0.5f);
+                }
+                st.p = count_below<NMETA>(meta, T);
+                if (!full_list && st.p >= kcols) flags |= 8;   // list continues past the staged columns
+                // TF32 split by truncation (the tensor core truncates fp32 operands to TF32):
+                // hi = x' with the low 13 bits cleared, lo = x' - hi (exact) passed as is
+                const uint32_t ab = sbase + L.aop + (uint32_t)((i % L.NA) * kTcRows * KT * 4);
+#pragma unroll
+                for (int j = 0; j < DP; j += 4) {
                     float h[4], l[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        h[i] = tc::tf32_rna(xc[4 * c + i]);
-                        l[i] = tc::tf32_rna(xc[4 * c + i] - h[i]);
+                    for (int q = 0; q < 4; ++q) {
+                        h[q] = __uint_as_float(__float_as_uint(xh[j + q]) & 0xFFFFE000u);
+                        l[q] = xh[j + q] - h[q];
                     }
-                    tc::sts128(aBase + tc::op_off(t, 4 * c, kTcRows), h[0], h[1], h[2], h[3]);
-                    tc::sts128(aBase + tc::op_off(t, DP + 4 * c, kTcRows), l[0], l[1], l[2], l[3]);
-                    tc::sts128(aBase + tc::op_off(t, 2 * DP + 4 * c, kTcRows), h[0], h[1], h[2], h[3]);
+                    tc::sts128(ab + tc::op_off(t, j, kTcRows), h[0], h[1], h[2], h[3]);
+                    tc::sts128(ab + tc::op_off(t, DP + j, kTcRows), l[0], l[1], l[2], l[3]);
+                    tc::sts128(ab + tc::op_off(t, 2 * DP + j, kTcRows), h[0], h[1], h[2], h[3]);
                 }
+                const float xxh = __uint_as_float(__float_as_uint(xx) & 0xFFFFE000u);
+                tc::sts128(ab + tc::op_off(t, 3 * DP, kTcRows), xxh, xx - xxh, 1.f, 1.f);
             }
-            if (A != colA) {                      // columns [A | NL[A][0..W-1)], cached while A repeats
-                for (int jj = t; jj < W; jj += kTcRows) {
-                    uint64_t key;
-                    if (jj == 0) key = ((uint64_t)__float_as_uint(-INFINITY) << 32) | (uint32_t)A;
-                    else key = jj - 1 < ks ? __ldg(p.NL + (int64_t)A * ks + (jj - 1)) : kSentinel;
-                    const int c = key_c(key);
-                    float cs = 0.f;
-#pragma unroll
-                    for (int j4 = 0; j4 < DP / 4; ++j4) {
-                        const float4 ca = Cn.ld(A, DP, 4 * j4), cj = Cn.ld(c, DP, 4 * j4);
-                        const float v[4] = {ca.x - cj.x, ca.y - cj.y, ca.z - cj.z, ca.w - cj.w};  // c_j - c_A
-                        float h[4], l[4];
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            cs = fmaf(v[i], v[i], cs);
-                            h[i] = tc::tf32_rna(v[i]);
-                            l[i] = tc::tf32_rna(v[i] - h[i]);
-                        }
-                        tc::sts128(bBase + tc::op_off(jj, 4 * j4, W), h[0], h[1], h[2], h[3]);
-                        tc::sts128(bBase + tc::op_off(jj, DP + 4 * j4, W), h[0], h[1], h[2], h[3]);
-                        tc::sts128(bBase + tc::op_off(jj, 2 * DP + 4 * j4, W), l[0], l[1], l[2], l[3]);
-                    }
-                    sKey[jj] = make_float4(key_h(key), __int_as_float(c), cs, 0.f);
-                }
-                colA = A;
-            }
+            st.flags = flags;
+            rstate[b * kTcRows + t] = st;
+            const int pw = (__reduce_max_sync(kFull, active ? min(st.p, kcols) : 0) + 15) & ~15;
+            if (lane == 0) s_info[b].pw[warp] = pw;
             tc::fence_async_smem();
-            tc::fence_before();
-            __syncthreads();                                               // (2)
-            tc::fence_after();
-            // ---- 3. MMA: D[128 x W] = A' . B'^T ----------------------------------------------
+            // the tile's MMA width: max over the four prep warps (named barrier among them)
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             if (t == 0) {
-#pragma unroll
-                for (int kb = 0; kb < KT / 8; ++kb)
-                    tc::mma_tf32(tmem, tc::sdesc(aBase + kb * kTcRows * 32), tc::sdesc(bBase + kb * W * 32),
-                                 idesc, kb > 0);
-                tc::mma_commit(mbar);
+                TcInfo &inf = s_info[b];
+                inf.tile = tile;
+                inf.A = A;
+                inf.bslot = L.NB == 2 ? mslot : 0;
+                inf.mslot = mslot;
+                inf.N = max(max(inf.pw[0], inf.pw[1]), max(inf.pw[2], inf.pw[3]));
             }
-            load(tile_next);                      // overlap the next tile's loads with the MMA
-            prefetched = true;
-            tc::mbar_wait(mbar, phase);
-            phase ^= 1;
-            tc::fence_after();
-            // ---- 4. epilogue: per-row best / second best over the taken columns (clauses 2/3 for
-            //      own rows, the triangle bound around A for misfits; never the row's own
-            //      cluster, which the direct tighten already evaluated)
-            int j0 = 0;
-            for (; j0 < W; j0 += 16) {
-                if (!__any_sync(kFull, active && sKey[j0].x < T)) break;
-                float v[16];
-                tc::tmem_ld16(tlane + (uint32_t)j0, v);
-                steps += 16;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float4 kk = sKey[j0 + i];
-                    const int c = __float_as_int(kk.y);
-                    const bool take = active && kk.x < T && c != aold;
-                    float q = fmaf(-2.f, v[i], xx + kk.z);
-                    q = take ? q : INFINITY;
-                    ns += (take && !misfit);
-                    q2 = fminf(q2, fmaxf(q, bq));
-                    bc = q < bq ? c : bc;
-                    bq = fminf(q, bq);
-                }
-            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             tc::fence_before();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[b]));
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) c_clause1 += __shfl_xor_sync(kFull, c_clause1, o);
+        if (lane == 0 && c_clause1) atomicAdd(p.counters + 2, c_clause1);
+    } else {
+        // ================= epilogue: best / second-best column, exact-mode decision ==========
+        const int ew = warp - kTcEpiWarp0;            // TMEM lane quadrant
+        const int r = ew * 32 + lane;                 // row within the tile
+        const uint32_t tlane = s_tmem + ((uint32_t)(ew * 32) << 16);
+        const float eps = *p.eps;
+        const float kappa = 2.f * (58.f + DP / 4.f + KT / 2.f) * 5.9604645e-8f;
+        CRow<CSMEM> Cn;
+        if constexpr (CSMEM) Cn.base = tc::smem_u32(sC); else Cn.base = p.Cneg;
+        double *acc = p.acc + (int64_t)(blockIdx.x % p.nslab) * k * (DP + 1);
+        RunAcc<DP> ra;
+        ra.clear();
+        unsigned long long c_changed = 0, c_dists = 0, c_refined = 0, c_cols = 0, c_fb = 0;
+        uint32_t qid[16];                             // column ids 0..15 kept in registers
+#pragma unroll
+        for (int q = 0; q < 16; ++q) { qid[q] = (uint32_t)q; asm volatile("" : "+r"(qid[q])); }
+        for (int i = 0;; ++i) {
+            const int s = i % S, b = i & 1;
+            tc::mbar_wait(tc::smem_u32(&s_accfull[b]), (uint32_t)((i >> 1) & 1));
+            tc::mbar_wait(tc::smem_u32(&s_aready[b]), (uint32_t)((i >> 1) & 1));   // acquire prep's writes
+            tc::fence_after();
+            const TcInfo inf = s_info[b];
+            if (inf.tile < 0) break;
+            const TcRow st = rstate[b * kTcRows + r];
+            const int64_t tile = inf.tile;
+            const int64_t row = tile * kTcRows + r;
+            const bool valid = st.flags & 1, active = st.flags & 2, misfit = st.flags & 4;
+            const bool uncovered = st.flags & 8;
+            const float4 *meta = meta0 + inf.mslot * NMETA;
+            const float *sx = reinterpret_cast<const float *>(smem + L.ring + s * L.stage_bytes);
+            float x[DP];
+#pragma unroll
+            for (int j = 0; j < DP; j += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(sx + r * DP + j);
+                x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+            }
+            const int pw = inf.N > 0 ? inf.pw[ew] : 0;
+            uint32_t m1 = 0x7fffffffu, m2 = 0x7fffffffu;   // packed keys: q bits, low byte = column
+            for (int c0 = 0; c0 < pw; c0 += 16) {
+                uint32_t rr[16];
+                tc::tmem_ld16(tlane + (uint32_t)(b * NMAX + c0), rr);
+                int kk[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q)      // key = q bits, low byte replaced by the column
+                    asm("lop3.b32 %0, %1, 0xFFFFFF00, %2, 0xEA;" : "=r"(kk[q]) : "r"(rr[q]), "r"(qid[q]));
+                int b1 = min(kk[0], min(kk[1], kk[2]));
+#pragma unroll
+                for (int q = 3; q < 16; q += 2) b1 = min(b1, min(kk[q], q + 1 < 16 ? kk[q + 1] : kk[q]));
+                // second best = min over the other keys: (k - b1 - 1) as unsigned maps b1 to the
+                // maximum and keeps the order of the rest (subtraction on the FMA pipe)
+                const uint32_t moff = ~(uint32_t)b1;  // -(b1 + 1)
+                uint32_t dd[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(dd[q]) : "r"(kk[q]), "r"(moff));
+                uint32_t d2 = min(dd[0], min(dd[1], dd[2]));
+#pragma unroll
+                for (int q = 3; q < 16; q += 2) d2 = min(d2, min(dd[q], q + 1 < 16 ? dd[q + 1] : dd[q]));
+                const uint32_t off = (uint32_t)b1 + 1u;
+                const int g1 = b1 + c0, g2 = (int)(d2 + off) + c0;        // globalise the column
+                const int n1 = min((int)m1, g1);
+                m2 = (uint32_t)min(max((int)m1, g1), min((int)m2, g2));
+                m1 = (uint32_t)n1;
+            }
+            if (lane == 0) c_cols += (unsigned long long)pw;
+            // everything this tile needs from the metadata slot, before releasing the buffers
+            const float cmax = pw > 0 ? meta[pw - 1].w : 0.f;
+            const int cc1 = m1 != 0x7fffffffu ? __float_as_int(meta[m1 & 0xff].y) : -1;
+            const int cc2 = m2 != 0x7fffffffu ? __float_as_int(meta[m2 & 0xff].y) : -1;
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_tfree[b]));   // TMEM / A / row state / metadata free
+            int anew = st.a;
+            float unew = st.uu;
             if (active) {
-                // the staged columns cover the row's candidates unless its prefix runs past them
-                const bool covered = !partial_cols || !(sKey[W - 1].x < T);
-                // every taken column has 2 H < 2 T, so |c'|^2 <= 4 T^2 (1 + 2^-20): one bound per row
-                const float E = kappa * fmaf(4.000004f * T, T, xx);
-                const float ub = __fadd_ru(__fsqrt_ru(__fadd_ru(bq, E)), eps);
-                const float lb2 = q2 < INFINITY ? __fsub_rd(__fsqrt_rd(fmaxf(__fsub_rd(q2, E), 0.f)), eps) : INFINITY;
-                walk = !covered || lb2 <= ub;            // TC-ambiguous or uncovered: direct walk
-                dbg_walk += walk;
-                dbg_uncov += !covered;
-                dbg_mis += misfit;
-                if (!walk && misfit) {
-                    // MTI distance count of this row: 1 + #{c : H[a][c] < ut} (binary search)
-                    const uint64_t *nl = p.NL + (int64_t)aold * ks;
-                    int lo = 0, hi = k - 1;
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (key_h(__ldg(nl + mid)) < ut) lo = mid + 1; else hi = mid;
+                bool fallback = uncovered;
+                const float E = __fmul_ru(kappa, __fadd_ru(st.xx, cmax));
+                // eps_C + centring roundings 2^-24 (|x'| + |c'|) (+ slack for the roots)
+                const float epsr = __fadd_ru(eps, __fmul_ru(1.2e-7f, __fadd_ru(sqrt_up(st.xx), sqrt_up(cmax))));
+                const int k1 = (int)m1, k2 = (int)m2;
+                // common case, in the squared domain: the best column's lower bound exceeds the own
+                // upper bound, i.e. v1 - E > (ut + epsr)^2 (v1: truncated key value <= the TC value)
+                const float ue = __fadd_ru(st.ut, epsr);
+                const float thr = __fadd_ru(__fmul_ru(ue, ue), E);
+                const bool stay_fast = !fallback && !misfit && (k1 == 0x7fffffff || __int_as_float(k1 & ~0xff) > thr);
+                if (stay_fast) {
+                    unew = st.ut;
+                } else if (!fallback) {
+                    // TC candidate intervals on the distance scale (key truncation: <= 2^-15 relative)
+                    auto U_of = [&](int key) {
+                        const float v = fmaxf(__int_as_float(key & ~0xff), 0.f);
+                        return __fadd_ru(sqrt_up(__fadd_ru(__fmul_ru(v, 1.0000306f), E)), epsr);
+                    };
+                    auto L_of = [&](int key) {
+                        if (key == 0x7fffffff) return INFINITY;
+                        const float v = __int_as_float(key & ~0xff);
+                        return fmaxf(0.f, __fsub_rd(sqrt_dn(fmaxf(__fsub_rd(v, E), 0.f)), epsr));
+                    };
+                    // own cluster: direct interval [lo, ut]; a misfit's own cluster is also a column
+                    float Uo = st.ut, Lo = st.lo, Ui = INFINITY, Li = INFINITY, Lother = INFINITY;
+                    int ci = -1;                               // best column other than the own cluster
+                    if (cc1 == st.a) {                         // (misfit) own is the best column: merge
+                        Uo = fminf(Uo, U_of(k1)); Lo = fmaxf(Lo, L_of(k1));
+                        ci = cc2;
+                        if (ci >= 0) { Ui = U_of(k2); Li = L_of(k2); Lother = -1.f; }   // third unknown
+                    } else {
+                        ci = cc1;
+                        if (ci >= 0) { Ui = U_of(k1); Li = L_of(k1); }
+                        Lother = L_of(k2);                     // (may be the own cluster's column)
                     }
-                    ns = 1 + lo;
+                    // misfit rows also have the tile cluster A (distance sqrt(xx), direct form)
+                    float UA = INFINITY, LA = INFINITY;
+                    if (misfit) { UA = upper_d(st.xx, p.g_up, eps); LA = lower_d(st.xx, p.g_dn, eps); }
+                    if (Uo < fminf(Li, LA)) {                                   // stays
+                        unew = Uo;
+                    } else if (misfit && UA < fminf(Lo, Li)) {                  // moves to A
+                        anew = inf.A; unew = UA;
+                    } else if (ci >= 0 && Ui < fminf(fminf(Lo, LA), Lother)) {  // moves to a column
+                        anew = ci; unew = Ui;
+                    } else {
+                        fallback = true;
+                    }
                 }
-            }
-        }
-        if (!prefetched) load(tile_next);
-
-        // ---- 5. rows left to the CUDA cores: direct-form walk + exact-mode decision ---------
-        int anew = aold;
-        float unew = uu;
-        if (active) {
-            if (walk) { bq = q_own; q2 = INFINITY; bc = aold; ns = 1; }
-            const uint64_t *nl = p.NL + (int64_t)aold * ks;
-            bool walking = walk;
-            if (__any_sync(__activemask(), walking)) {
-                ulonglong2 kp = walking ? __ldg(reinterpret_cast<const ulonglong2 *>(nl)) : make_ulonglong2(kSentinel, kSentinel);
-                for (int j = 0;; j += 2) {
-                    const bool w0 = walking && key_h(kp.x) < ut;
-                    const bool w1 = w0 && key_h(kp.y) < ut;
-                    if (!__any_sync(__activemask(), w0)) break;
-                    steps += 2;
-                    const ulonglong2 np = w1 ? __ldg(reinterpret_cast<const ulonglong2 *>(nl + j + 2)) : make_ulonglong2(kSentinel, kSentinel);
-                    const int c0 = key_c(kp.x), c1 = key_c(kp.y);
-                    float qa = dist2<DP, CSMEM>(x, Cn, c0);
-                    float qb = dist2<DP, CSMEM>(x, Cn, c1);
-                    qa = w0 ? qa : INFINITY;
-                    qb = w1 ? qb : INFINITY;
-                    ns += (int)w0 + (int)w1;
-                    q2 = fminf(q2, fmaxf(qa, bq)); bc = qa < bq ? c0 : bc; bq = fminf(qa, bq);
-                    q2 = fminf(q2, fmaxf(qb, bq)); bc = qb < bq ? c1 : bc; bq = fminf(qb, bq);
-                    walking = w1;
-                    kp = np;
+                if (fallback) {
+                    // CUDA-core MTI walk over NL[a] in the direct form + exact-mode refinement
+                    ++c_fb;
+                    const uint64_t *nl = p.NL + (int64_t)st.a * p.ks;
+                    float bq = dist2<DP, CSMEM>(x, Cn, st.a), q2 = INFINITY;
+                    int bc = st.a;
+                    for (int j = 0; j < k - 1; ++j) {
+                        const uint64_t key = __ldg(nl + j);
+                        if (!(key_h(key) < st.ut)) break;
+                        const int c = key_c(key);
+                        const float q = dist2<DP, CSMEM>(x, Cn, c);
+                        q2 = fminf(q2, fmaxf(q, bq));
+                        bc = q < bq ? c : bc;
+                        bq = fminf(q, bq);
+                    }
+                    const float ub = upper_d(bq, p.g_up, eps);
+                    if (q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub) {
+                        anew = refine64(sx + r * DP, p.d, p.C64, k, st.a, nl, st.ut, &unew);
+                        ++c_refined;
+                    } else {
+                        anew = bc;
+                        unew = ub;
+                    }
                 }
+                // MTI distance count 1 (tighten) + #{c : H[a][c] < u_t}: from the tile's columns
+                // for rows of A; misfit / uncovered rows are counted by k_mti_count after the pass
+                if (!misfit && !uncovered) c_dists += (unsigned long long)(1 + st.p);
             }
-            if (walk) {
-                const float ub = upper_d(bq, p.g_up, eps);
-                const bool amb = q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub;
-                if (amb) {
-                    anew = refine64(p.X + row * DP, p.d, p.C64, k, aold, nl, ut, &unew);
-                    ++c_refined;
-                } else {
-                    anew = bc;
-                    unew = ub;
-                }
-            } else {
-                anew = bc;
-                // tight bound for the next pass: direct-form distance to the winner
-                unew = bc == aold ? ut : upper_d(dist2<DP, CSMEM>(x, Cn, bc), p.g_up, eps);
+            {   // deferred counts: compacted per warp into defer[tile*128 + ew*32 + i], count dcount[tile*4 + ew]
+                const bool defer = active && (misfit || uncovered);
+                const unsigned dm = __ballot_sync(kFull, defer);
+                if (defer)
+                    p.defer[tile * kTcRows + ew * 32 + __popc(dm & ((1u << lane) - 1u))] =
+                        ((unsigned long long)(uint32_t)st.a << 32) | __float_as_uint(st.ut);
+                if (lane == 0) p.dcount[tile * 4 + ew] = __popc(dm);
             }
-            c_dists += (unsigned long long)ns;
+            if (valid) {
+                p.a[row] = anew;
+                p.u[row] = unew;
+                c_changed += (anew != st.a);
+            }
+            reduce_batch<DP>(ra, x, anew, valid, acc, p.d, lane);
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_sfree[s]));     // stage reusable
         }
-        if (valid) {
-            p.a[row] = anew;
-            p.u[row] = unew;
-            c_changed += (anew != aold);
-        }
-        reduce_batch<DP>(ra, x, anew, valid, acc, p.d, lane);
-        tile = tile_next;
-        ++it;
-    }
-    ra.flush(acc, p.d, lane);
+        ra.flush(acc, p.d, lane);
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        c_changed += __shfl_xor_sync(kFull, c_changed, o);
-        c_dists += __shfl_xor_sync(kFull, c_dists, o);
-        c_clause1 += __shfl_xor_sync(kFull, c_clause1, o);
-        c_refined += __shfl_xor_sync(kFull, c_refined, o);
+        for (int o = 16; o >= 1; o >>= 1) {
+            c_changed += __shfl_xor_sync(kFull, c_changed, o);
+            c_dists += __shfl_xor_sync(kFull, c_dists, o);
+            c_refined += __shfl_xor_sync(kFull, c_refined, o);
+            c_fb += __shfl_xor_sync(kFull, c_fb, o);
+        }
+        if (lane == 0) {
+            if (c_changed) atomicAdd(p.counters + 0, c_changed);
+            if (c_dists) atomicAdd(p.counters + 1, c_dists);
+            if (c_refined) atomicAdd(p.counters + 3, c_refined);
+            if (c_cols) atomicAdd(p.counters + 4, c_cols);
+            if (c_fb) atomicAdd(p.counters + 5, c_fb);
+        }
     }
-    if (lane == 0) {
-        if (c_changed) atomicAdd(p.counters + 0, c_changed);
-        if (c_dists) atomicAdd(p.counters + 1, c_dists);
-        if (c_clause1) atomicAdd(p.counters + 2, c_clause1);
-        if (c_refined) atomicAdd(p.counters + 3, c_refined);
-        if (steps) atomicAdd(p.counters + 4, (unsigned long long)steps);
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        dbg_walk += __shfl_xor_sync(kFull, dbg_walk, o);
-        dbg_uncov += __shfl_xor_sync(kFull, dbg_uncov, o);
-        dbg_mis += __shfl_xor_sync(kFull, dbg_mis, o);
-    }
-    if (lane == 0) {
-        atomicAdd(p.counters + 5, (unsigned long long)dbg_walk);
-        atomicAdd(p.counters + 6, (unsigned long long)dbg_uncov);
-        atomicAdd(p.counters + 7, (unsigned long long)dbg_mis);
-    }
+    __syncwarp();
     tc::fence_before();
     __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(p.tmem_cols));
+    if (warp == kTcMmaWarp)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(s_tmem), "r"(p.tmem_cols));
 }
 
-size_t tc_smem(int DP, bool csmem, int k, int W)
+// MTI distance counts of the rows the tensor-core pass deferred (misfit / uncovered rows):
+// counters[1] += sum over entries (a, u_t) of 1 + #{c : H[a][c] < u_t}  (binary search in NL[a]);
+// entries of (tile g, warp w) are defer[g*128 + w*32 .. + dcount[g*4 + w]).  One warp per pair.
+__global__ void k_mti_count(const unsigned long long *defer, const int *dcount, int64_t ntiles,
+                            unsigned long long *counters, const uint64_t *NL, int ks, int k)
 {
-    const int KT = 3 * DP;
-    return (size_t)kTcRows * KT * 4 + (size_t)W * KT * 4 + (size_t)W * 16 +
-           (size_t)((csmem ? k * DP : 0) + 2 * k) * 4;
+    const int lane = threadIdx.x & 31;
+    unsigned long long sum = 0;
+    for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ntiles * 4;
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int cnt = dcount[g];
+        if (lane < cnt) {
+            const unsigned long long e = defer[g * 32 + lane];
+            const int a = (int)(e >> 32);
+            const float ut = __uint_as_float((uint32_t)e);
+            sum += 1 + count_below_nl(NL + (int64_t)a * ks, k - 1, ut);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+    if (lane == 0 && sum) atomicAdd(counters + 1, sum);
 }
 
-template <int DP, bool CSMEM>
-static cudaError_t launch_tc_t(const AssignParams &p, int grid, cudaStream_t st)
+cudaError_t launch_mti_count(const unsigned long long *defer, const int *dcount, int64_t ntiles,
+                             unsigned long long *counters, const uint64_t *NL, int ks, int k, int num_sms,
+                             cudaStream_t st)
 {
-    const size_t sm = tc_smem(DP, CSMEM, p.k, p.W);
-    cudaError_t e = cudaFuncSetAttribute(k_mti_tc<DP, CSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_mti_count<<<num_sms * 8, 256, 0, st>>>(defer, dcount, ntiles, counters, NL, ks, k);
+    return cudaGetLastError();
+}
+
+// ---- host side: pipeline configuration, residency, launch ---------------------------------
+// Deepest pipeline that fits: prefer 2 CTAs per SM, then ring depth, A/B double buffering.
+static TcCfg pick_cfg(int DP, bool csmem, int k, int nmax, int optin, int smem_sm, int *ctas)
+{
+    const int static_bytes = 1024;
+    for (int want = 2; want >= 1; --want) {
+        const int budget = std::min(optin, smem_sm / want - 1024) - static_bytes;
+        for (int S : {4, 3, 2})
+            for (int NA : {2, 1})
+                for (int NB : {2, 1}) {
+                    TcCfg L = tc_cfg(DP, csmem, k, nmax, S, NA, NB);
+                    if (L.total <= budget) { *ctas = want; return L; }
+                }
+    }
+    *ctas = 0;
+    return tc_cfg(DP, csmem, k, nmax, 2, 1, 1);
+}
+
+template <int DP, bool CSMEM, int NMETA>
+static cudaError_t launch_tc_t(const AssignParams &p, const TcCfg &L, int grid, cudaStream_t st)
+{
+    cudaError_t e = cudaFuncSetAttribute(k_mti_tc<DP, CSMEM, NMETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
     if (e != cudaSuccess) return e;
-    k_mti_tc<DP, CSMEM><<<grid, kTcRows, sm, st>>>(p);
+    k_mti_tc<DP, CSMEM, NMETA><<<grid, kTcThreads, L.total, st>>>(p, L);
     return cudaGetLastError();
 }
 
 template <int DP, bool CSMEM>
-static int tc_grid_t(int k, int W, int tmem_cols, int num_sms)
+static cudaError_t launch_tc_m(const AssignParams &p, const TcCfg &L, int grid, cudaStream_t st)
 {
-    const size_t sm = tc_smem(DP, CSMEM, k, W);
-    cudaError_t e1 = cudaFuncSetAttribute(k_mti_tc<DP, CSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    int per_sm = 0;
-    cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mti_tc<DP, CSMEM>, kTcRows, sm);
-    // The occupancy API reports 1 CTA/SM for kernels that allocate TMEM; compute the residency
-    // from registers, shared memory and TMEM columns instead.
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_mti_tc<DP, CSMEM>);
-    int dev = 0, smem_sm = 0, regs_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-    const int regs_cta = ((fa.numRegs + 7) & ~7) * kTcRows;
-    const int by_regs = regs_sm / std::max(1, regs_cta);
-    const int by_smem = smem_sm / (int)(sm + fa.sharedSizeBytes + 1024);
-    const int by_tmem = 512 / tmem_cols;
-    const int calc = std::min(std::min(by_regs, by_smem), std::min(by_tmem, 16));
-    if (getenv("KM_DEBUG"))
-        fprintf(stderr, "[km] tc grid: DP=%d smem=%zu W=%d cols=%d occ_api=%d regs=%d by_regs=%d by_smem=%d by_tmem=%d -> %d (%s/%s)\n",
-                DP, sm, W, tmem_cols, per_sm, fa.numRegs, by_regs, by_smem, by_tmem, calc,
-                cudaGetErrorString(e1), cudaGetErrorString(e2));
-    per_sm = calc;
-    return std::max(1, per_sm) * num_sms;
-}
-
-bool tc_supported(int DP) { return DP == 8 || DP == 16 || DP == 32; }
-
-cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st)
-{
-    switch (DP * 2 + (csmem ? 1 : 0)) {
-    case 16: return launch_tc_t<8, false>(p, grid, st);
-    case 17: return launch_tc_t<8, true>(p, grid, st);
-    case 32: return launch_tc_t<16, false>(p, grid, st);
-    case 33: return launch_tc_t<16, true>(p, grid, st);
-    case 64: return launch_tc_t<32, false>(p, grid, st);
-    case 65: return launch_tc_t<32, true>(p, grid, st);
+    switch (p.nmeta) {
+    case 16: return launch_tc_t<DP, CSMEM, 16>(p, L, grid, st);
+    case 32: return launch_tc_t<DP, CSMEM, 32>(p, L, grid, st);
+    case 64: return launch_tc_t<DP, CSMEM, 64>(p, L, grid, st);
+    case 128: return launch_tc_t<DP, CSMEM, 128>(p, L, grid, st);
+    case 256: return launch_tc_t<DP, CSMEM, 256>(p, L, grid, st);
     }
     return cudaErrorInvalidValue;
 }
 
-int mti_tc_grid(int DP, bool csmem, int k, int W, int tmem_cols, int num_sms)
+bool tc_supported(int DP) { return DP == 8 || DP == 16 || DP == 32; }
+
+int tc_kt_host(int DP) { return tc_kt(DP); }
+
+int tc_nmeta_host(int nmax) { return tc_nmeta(nmax); }
+
+// shared memory the tensor-core pass needs (0 if it does not fit one CTA) and its grid
+size_t tc_plan(int DP, bool csmem, int k, int nmax, int num_sms, int *grid, int *tmem_cols)
 {
+    int dev = 0, optin = 0, smem_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    int ctas = 0;
+    TcCfg L = pick_cfg(DP, csmem, k, nmax, optin, smem_sm, &ctas);
+    int cols = 32;
+    while (cols < 2 * nmax) cols <<= 1;
+    ctas = std::min(ctas, 512 / cols);
+    *tmem_cols = cols;
+    *grid = std::max(1, ctas) * num_sms;
+    if (getenv("KM_DEBUG"))
+        fprintf(stderr, "[km] tc plan: DP=%d k=%d nmax=%d S=%d NA=%d NB=%d smem=%d cols=%d ctas/SM=%d\n",
+                DP, k, nmax, L.S, L.NA, L.NB, L.total, cols, ctas);
+    return ctas > 0 ? (size_t)L.total : 0;
+}
+
+cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st)
+{
+    int dev = 0, optin = 0, smem_sm = 0, ctas = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const TcCfg L = pick_cfg(DP, csmem, p.k, p.nmax, optin, smem_sm, &ctas);
+    if (ctas == 0) return cudaErrorInvalidValue;
     switch (DP * 2 + (csmem ? 1 : 0)) {
-    case 16: return tc_grid_t<8, false>(k, W, tmem_cols, num_sms);
-    case 17: return tc_grid_t<8, true>(k, W, tmem_cols, num_sms);
-    case 32: return tc_grid_t<16, false>(k, W, tmem_cols, num_sms);
-    case 33: return tc_grid_t<16, true>(k, W, tmem_cols, num_sms);
-    case 64: return tc_grid_t<32, false>(k, W, tmem_cols, num_sms);
-    case 65: return tc_grid_t<32, true>(k, W, tmem_cols, num_sms);
+    case 16: return launch_tc_m<8, false>(p, L, grid, st);
+    case 17: return launch_tc_m<8, true>(p, L, grid, st);
+    case 32: return launch_tc_m<16, false>(p, L, grid, st);
+    case 33: return launch_tc_m<16, true>(p, L, grid, st);
+    case 64: return launch_tc_m<32, false>(p, L, grid, st);
+    case 65: return launch_tc_m<32, true>(p, L, grid, st);
     }
-    return num_sms;
+    return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------------------
+// S1 (tensor-core part): per cluster c, the B operand block and column metadata of its
+// neighbour list (ascending H, as NL[c]); run after k_prep (which built NL).
+//   B row j (column c_j = NL[c][j]): c' = fp32(C[c_j]) - fp32(C[c]) (RN), split TF32 hi/lo:
+//     [-2 c'hi | -2 c'hi | -2 c'lo | 1 | 1 | cc_hi | cc_lo | 0 ..],  cc = |c'|^2
+//   meta j: {H (fp32, rounded down), c_j bits, |c'|^2 rounded up, prefix max of that}
+//   columns past the k-1 neighbours: q = xx + 1e30 (never a winner), meta {NaN, c, 0, prefix}
+__global__ void k_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
+                          float *Bop, float4 *Bmeta)
+{
+    const int nmeta = tc_nmeta(nmax);
+    extern __shared__ float4 smeta[];
+    const int c = blockIdx.x, KT = tc_kt(DP);
+    const double *Cc = C + (int64_t)c * d;
+    const uint64_t *nl = NL + (int64_t)c * ks;
+    float *B = Bop + (int64_t)c * nmax * KT;
+    for (int j = threadIdx.x; j < nmax; j += blockDim.x) {
+        const bool real = j < k - 1;
+        const int cj = real ? key_c(nl[j]) : c;
+        const double *Cj = C + (int64_t)cj * d;
+        double cn2 = 0.0;
+        for (int e = 0; e < DP; ++e) {
+            const float v = e < d ? __fsub_rn((float)Cj[e], (float)Cc[e]) : 0.f;
+            const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(__fsub_rn(v, hi));
+            cn2 += (double)v * (double)v;
+            B[tc::op_off(j, e, nmax) / 4] = real ? -2.f * hi : 0.f;
+            B[tc::op_off(j, DP + e, nmax) / 4] = real ? -2.f * hi : 0.f;
+            B[tc::op_off(j, 2 * DP + e, nmax) / 4] = real ? -2.f * lo : 0.f;
+        }
+        const float ccf = real ? (float)cn2 : 1e30f;
+        const float cch = tc::tf32_rna(ccf);
+        const float ccl = real ? tc::tf32_rna((float)(cn2 - (double)cch)) : 0.f;
+        B[tc::op_off(j, 3 * DP, nmax) / 4] = 1.f;
+        B[tc::op_off(j, 3 * DP + 1, nmax) / 4] = 1.f;
+        B[tc::op_off(j, 3 * DP + 2, nmax) / 4] = cch;
+        B[tc::op_off(j, 3 * DP + 3, nmax) / 4] = ccl;
+        for (int e = 3 * DP + 4; e < KT; ++e) B[tc::op_off(j, e, nmax) / 4] = 0.f;
+        smeta[j] = make_float4(real ? key_h(nl[j]) : __int_as_float(0x7fc00000), __int_as_float(cj),
+                               real ? __double2float_ru(cn2 * (1.0 + 1e-12)) : 0.f, 0.f);
+    }
+    __syncthreads();
+    for (int j = nmax + threadIdx.x; j < nmeta; j += blockDim.x)
+        smeta[j] = make_float4(__int_as_float(0x7fc00000), __int_as_float(c), 0.f, 0.f);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int j = 0; j < nmeta; ++j) { m = fmaxf(m, smeta[j].z); smeta[j].w = m; }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nmeta; j += blockDim.x) Bmeta[(int64_t)c * nmeta + j] = smeta[j];
+}
+
+cudaError_t launch_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
+                           float *Bop, float4 *Bmeta, cudaStream_t st)
+{
+    k_prep_tc<<<k, 128, (size_t)tc_nmeta(nmax) * sizeof(float4), st>>>(C, NL, k, d, DP, ks, nmax, Bop, Bmeta);
+    return cudaGetLastError();
 }
 
 }  // namespace km

@@ -87,7 +87,7 @@ def test_B3_half_factor_on_gpu():
 
 
 # ---- seeded configs, free-running (strict tier) -------------------------------------------
-@pytest.mark.parametrize("prune,engine", [("mti", "auto"), ("mti", "cuda"), ("none", "auto")])
+@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("none", "auto")])
 def test_c1_free_running(prune, engine):
     X, idx, _ = make_config("c1")
     C0 = X[idx].astype(float)
@@ -102,7 +102,7 @@ def test_c1_free_running(prune, engine):
         assert np.all(np.abs(gc - r.clause1) <= 1e-3 * 10000 + 1)
 
 
-@pytest.mark.parametrize("prune,engine", [("mti", "auto"), ("mti", "cuda"), ("none", "auto")])
+@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("none", "auto")])
 def test_c2_free_running(prune, engine):
     X, idx, _ = make_config("c2")
     C0 = X[idx].astype(float)
@@ -114,7 +114,7 @@ def test_c2_free_running(prune, engine):
         assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
-@pytest.mark.parametrize("engine", ["auto", "cuda"])
+@pytest.mark.parametrize("engine", ["tensor", "cuda"])
 @pytest.mark.parametrize("name,n,iters", [("c3", 2_000_000, 30), ("c4", 1_000_000, 30)])
 def test_spectral_shaped_free_running(name, n, iters, engine):
     X, idx, _ = make_config(name, n=n)
@@ -126,7 +126,7 @@ def test_spectral_shaped_free_running(name, n, iters, engine):
     assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
-@pytest.mark.parametrize("engine", ["auto", "cuda"])
+@pytest.mark.parametrize("engine", ["tensor", "cuda"])
 def test_c5_shaped_large_k(engine):
     X, idx, _ = make_config("c5", n=300_000)
     C0 = X[idx].astype(float)
