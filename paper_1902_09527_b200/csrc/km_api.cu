@@ -139,6 +139,13 @@ struct km_ctx {
     // tensor-core MTI engine: per-cluster B operand blocks, column metadata, NL ranks
     float *Bop = nullptr;
     float4 *Bmeta = nullptr;
+    // walk engine: per-cluster candidate rows and H
+    float4 *Wblk = nullptr;
+    float *Wcc = nullptr, *WH = nullptr;
+    float2 *Wmeta = nullptr;
+    bool wh_smem = false;
+    int wpad = 0, whs = 0, wbits = 0, walk_grid = 0;
+    bool use_walk = false;
     unsigned long long *defer = nullptr;   // deferred distance-count entries (n_alloc)
     int *dcount = nullptr;                 // per 128-row tile
     bool use_tc = false;
@@ -148,6 +155,8 @@ struct km_ctx {
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     double *acc = nullptr;          // k x (DP+1) reduced sums | counts (allreduce buffer)
+    double *S = nullptr;            // k x (DP+1) running sums | counts (delta passes add to it)
+    bool delta_pass = false;        // this iteration's pass reduced only the moves
     double *acc_part = nullptr;     // grid x k x (DP+1) per-CTA partials
     int part_grid = 0;
     int nslab = 0;                  // number of partial slabs (= SM count)
@@ -188,6 +197,11 @@ km_status prep(km_ctx *c)
     p.eps_bits = c->eps_bits;
     KM_CUDA(km::launch_prep(p, c->st));
     c->launches += 1;
+    if (c->use_walk) {
+        KM_CUDA(km::launch_prep_walk(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->wpad, c->whs, c->Wblk, c->Wcc, c->Wmeta, c->WH,
+                                     c->st));
+        c->launches += 1;
+    }
     if (c->use_tc) {
         KM_CUDA(km::launch_prep_tc(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->tc_nmax, c->Bop, c->Bmeta, c->st));
         c->launches += 1;
@@ -226,14 +240,23 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
     p.defer = c->defer;
     p.dcount = c->dcount;
     p.nmeta = c->use_tc ? km::tc_nmeta_host(c->tc_nmax) : 0;
+    p.Wblk = c->Wblk;
+    p.WH = c->WH;
+    p.Wcc = c->Wcc;
+    p.Wmeta = c->Wmeta;
+    p.wh_smem = c->wh_smem ? 1 : 0;
+    p.whs = c->whs;
+    p.wpad = c->wpad;
+    p.wbits = c->wbits;
     return p;
 }
 
 km_status launch_assign(km_ctx *c, int mode, int work_slot)
 {
     km::AssignParams p = assign_params(c, work_slot);
-    if (mode == km::MODE_MTI_REDUCE && c->use_tc) {
-        KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
+    if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
+        if (c->use_tc) KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
+        else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->st));
         KM_CUDA(km::launch_mti_count(c->defer, c->dcount, c->n_alloc / 128, c->counters, c->NL, c->ks, c->k,
                                      c->num_sms, c->st));
         c->launches += 1;
@@ -323,6 +346,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
     KM_TRY(prep(c));
     KM_CUDA(cudaEventRecord(ev[2], c->st));
+    c->delta_pass = !first && c->use_walk;
     if (first) {
         KM_TRY(launch_assign(c, km::MODE_DENSE, 0));
         KM_CUDA(cudaEventRecord(ev[3], c->st));
@@ -338,7 +362,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     KM_CUDA(cudaEventRecord(ev[4], c->st));
     KM_TRY(allreduce(c));
     KM_CUDA(cudaEventRecord(ev[5], c->st));
-    KM_CUDA(km::launch_update(c->acc, c->C, c->Cprev, c->k, c->d, c->DP, c->empty, c->st));
+    KM_CUDA(km::launch_update(c->acc, c->S, c->delta_pass ? 1 : 0, c->C, c->Cprev, c->k, c->d, c->DP, c->empty, c->st));
     c->launches += 1;
     KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, c->st));
@@ -383,8 +407,8 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
-    cudaFree(c->counters_g); cudaFree(c->acc_part);
+    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
+    cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
     if (c->comm) { NcclApi *N = nccl(); if (N) N->CommDestroy(c->comm); }
@@ -462,6 +486,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     c->eps_bits = reinterpret_cast<unsigned *>(ints + 1);
     c->work = ints + 2;   // two work counters
     KM_TRY(dalloc(&c->counters_g, 8));
+    KM_TRY(dalloc(&c->S, (size_t)k * (DP + 1)));
     KM_TRY(dalloc(&c->sse_buf, 1));
     KM_CUDA(cudaMallocHost(&c->hstat, sizeof(HostStat)));
     // points -> private padded copy
@@ -499,7 +524,6 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     }
     // the tensor-core kernel handles rows outside the tile's cluster without extra walks, so
     // re-bucketing only pays when the layout is badly mixed
-    if (c->use_tc && !(o->resort_fraction > 0.f)) c->resort_fraction = 0.5f;
     if (c->use_tc) {
         c->tc_nmax = std::min(256, std::max(16, (k - 1 + 15) & ~15));   // columns: NL[A] prefix
         if (const char *e = getenv("KM_TC_NMAX")) c->tc_nmax = std::max(16, std::min(c->tc_nmax, atoi(e) & ~15));
@@ -513,10 +537,34 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         const int KT = km::tc_kt_host(DP);
         KM_TRY(dalloc(&c->Bop, (size_t)k * c->tc_nmax * KT));
         KM_TRY(dalloc(&c->Bmeta, (size_t)k * km::tc_nmeta_host(c->tc_nmax)));
-        KM_TRY(dalloc(&c->defer, (size_t)c->n_alloc));
-        KM_TRY(dalloc(&c->dcount, (size_t)(c->n_alloc / 128) * 4));
         c->part_grid = std::max(c->part_grid, c->tc_grid);
     }
+    // CUDA-core engine: the centred expansion-form walk (k_walk); KM_LEGACY_WALK=1 keeps the
+    // direct-form lane walk of k_assign for A/B comparison
+    c->use_walk = !c->use_tc && c->prune == KM_PRUNE_MTI && k >= 2 && km::walk_supported(DP) &&
+                  !getenv("KM_LEGACY_WALK");
+    if (c->use_walk) {
+        c->wpad = (k + 1) & ~1;                    // k-1 neighbours + >= 1 dummy row, even
+        c->wbits = 1;
+        while ((1 << c->wbits) < c->wpad) ++c->wbits;
+        c->whs = 2;
+        while (c->whs < c->wpad) c->whs <<= 1;
+        c->wh_smem = (size_t)k * c->whs * sizeof(float) <= 64 * 1024;
+        KM_TRY(dalloc(&c->Wblk, (size_t)k * (c->wpad / 2) * (DP / 2)));
+        KM_TRY(dalloc(&c->Wcc, (size_t)k * c->wpad));
+        KM_TRY(dalloc(&c->Wmeta, (size_t)k * c->wpad));
+        KM_TRY(dalloc(&c->WH, (size_t)k * c->whs));
+        c->walk_grid = km::walk_grid(DP, c->csmem, k, c->whs, c->wh_smem, c->num_sms);
+        c->part_grid = std::max(c->part_grid, c->walk_grid);
+    }
+    if (c->use_tc || c->use_walk) {
+        KM_TRY(dalloc(&c->defer, (size_t)c->n_alloc));
+        KM_TRY(dalloc(&c->dcount, (size_t)(c->n_alloc / 32)));
+        KM_CUDA(cudaMemsetAsync(c->dcount, 0, (size_t)(c->n_alloc / 32) * sizeof(int), c->st));
+    }
+    // engines that handle rows outside the warp's / tile's cluster by the triangle bound only
+    // re-bucket when the layout is badly mixed
+    if ((c->use_tc || c->use_walk) && !(o->resort_fraction > 0.f)) c->resort_fraction = 0.25f;
     c->nslab = std::min(c->part_grid, c->num_sms);
     KM_TRY(dalloc(&c->acc_part, (size_t)c->nslab * k * (DP + 1)));
     if (c->world > 1) {

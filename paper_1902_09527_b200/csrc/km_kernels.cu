@@ -392,23 +392,32 @@ cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems,
 
 // ---------------------------------------------------------------------------------------
 // S4: C_new[c] = sums[c] / count[c] (IEEE fp64 division), or C_old[c] when empty (A10).
-__global__ void k_update(const double *acc, double *C, double *Cprev, int k, int d, int DP, int *empty)
+// S holds the running per-cluster sums | count: delta = 0 -> S = acc (full reduction of this
+// pass), delta = 1 -> S += acc (acc holds only the moves of this pass).
+__global__ void k_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
+                         int DP, int *empty)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)k * d) return;
-    int c = (int)(i / d), j = (int)(i % d);
-    double cnt = acc[(int64_t)c * (DP + 1) + DP];
-    double old = C[i];
-    Cprev[i] = old;
-    C[i] = cnt > 0.0 ? acc[(int64_t)c * (DP + 1) + j] / cnt : old;
-    if (j == 0 && !(cnt > 0.0)) atomicAdd(empty, 1);
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;     // one thread per cluster
+    if (c >= k) return;
+    double *Sc = S + (int64_t)c * (DP + 1);
+    const double *ac = acc + (int64_t)c * (DP + 1);
+    const double cnt = delta ? Sc[DP] + ac[DP] : ac[DP];
+    Sc[DP] = cnt;
+    if (!(cnt > 0.5)) atomicAdd(empty, 1);
+    for (int j = 0; j < d; ++j) {
+        const double v = delta ? Sc[j] + ac[j] : ac[j];
+        Sc[j] = v;
+        const int64_t ci = (int64_t)c * d + j;
+        const double old = C[ci];
+        Cprev[ci] = old;
+        C[ci] = cnt > 0.5 ? v / cnt : old;
+    }
 }
 
-cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, int d, int DP,
-                          int *empty, cudaStream_t st)
+cudaError_t launch_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
+                          int DP, int *empty, cudaStream_t st)
 {
-    int64_t tot = (int64_t)k * d;
-    k_update<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(acc, C, Cprev, k, d, DP, empty);
+    k_update<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(acc, S, delta, C, Cprev, k, d, DP, empty);
     return cudaGetLastError();
 }
 

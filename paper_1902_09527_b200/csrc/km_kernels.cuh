@@ -58,6 +58,15 @@ struct AssignParams {
     unsigned long long *defer;   // n_alloc: (a << 32 | u_t bits) of rows whose distance count is deferred
     int *dcount;           // ntiles: deferred entries per 128-row tile
     int32_t nmeta;         // Bmeta entries per cluster (power of two >= nmax, NaN padded)
+    // CUDA-core walk engine (k_walk, km_walk.cu)
+    const float4 *Wblk;    // k x wpad/2 x DP/2: per-cluster candidate pairs, -2 c' interleaved by row
+    const float *Wcc;      // k x wpad: |c'|^2 of the candidate rows
+    const float2 *Wmeta;   // k x wpad: {prefix max of |c'|^2 (up), centroid bits}
+    const float *WH;       // k x whs: H of the candidate rows (NaN past the list)
+    int32_t whs;           // WH row stride (power of two >= wpad)
+    int32_t wh_smem;       // 1: stage WH in shared memory
+    int32_t wpad;          // candidate rows per cluster (>= k, even)
+    int32_t wbits;         // key index bits (2^wbits >= wpad)
 };
 
 struct PrepParams {
@@ -101,8 +110,13 @@ cudaError_t launch_mti_count(const unsigned long long *defer, const int *dcount,
                              unsigned long long *counters, const uint64_t *NL, int ks, int k, int num_sms,
                              cudaStream_t st);
 int tc_nmeta_host(int nmax);
-cudaError_t launch_update(const double *acc, double *C, double *Cprev, int k, int d, int DP,
-                          int *empty, cudaStream_t st);
+bool walk_supported(int DP);
+cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st);
+int walk_grid(int DP, bool csmem, int k, int kp, bool whs, int num_sms);
+cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int kp, int whs,
+                             float4 *Wblk, float *Wcc, float2 *Wmeta, float *WH, cudaStream_t st);
+cudaError_t launch_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
+                          int DP, int *empty, cudaStream_t st);
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches);
 cudaError_t launch_sse(const float *X, const int32_t *a, const double *C, int64_t n, int d,
                        int DP, double *out, cudaStream_t st);

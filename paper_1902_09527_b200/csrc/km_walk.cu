@@ -1,0 +1,506 @@
+// km_walk.cu — CUDA-core MTI assignment pass ("walk" engine) + fused fp64 reduction, sm_100a.
+//
+// Method: PAPER.md §3.3 (1026-1053): u += f(a) (drift, 1028-1030); clause 1 (u <= s(a): keep,
+// no distance, 1036-1040); tighten U(u) = d(x, C[a]) (1033-1034); clauses 2/3: candidates c'
+// with 1/2 d(a, c') < u (1042-1053, readings A1/A5/A6 of DESIGN.md); per-cluster sums fused
+// into the same pass (§3.2, 1000-1011).  DESIGN.md "Walk engine".
+//
+// B200 realisation.  Rows are stored bucketed by cluster, so the 32 rows of a warp mostly share
+// one cluster A (the cluster of lane 16).  Every lane walks A's neighbour list (ascending H)
+// in lockstep, so each candidate row is ONE broadcast load for the warp:
+//   * distances in the centred expansion form q_j = |x'|^2 + |c'_j|^2 - 2 x'.c'_j with
+//     x' = x - C^[A], c'_j = C^[c_j] - C^[A] (k_prep_walk stores [-2 c'_j | |c'_j|^2, prefix
+//     max, H, c_j] per candidate): DP/2 + 2 FMA-pipe instructions per candidate instead of the
+//     2 DP of the direct form;
+//   * lanes of A stop at their own prefix p = #{j : H[A][j] < u_t} (clauses 2/3); a lane of
+//     another cluster a (a "misfit") takes the prefix H[A][j] < (u_t + d(x, A)) / 2: by the
+//     triangle inequality no centroid outside it can beat a, and a itself is inside it;
+//   * the warp evaluates up to its largest prefix; values past a lane's own prefix are true
+//     distances of real centroids, so they never change the argmin (only the error bound,
+//     which covers every evaluated column);
+//   * best / second-best by packed keys (q bits, low bits = position) with integer min/max;
+//   * exact mode: rigorous intervals decide the winner, otherwise the lane re-walks its own
+//     list in the direct form with fp64 refinement (same decision procedure as k_assign).
+// Distance counts (1 + #{c : H[a][c] < u_t}) of misfit lanes are deferred to k_mti_count.
+#include <cstdio>
+#include <cstdlib>
+
+#include "km_device.cuh"
+#include "km_kernels.cuh"
+
+namespace km {
+
+constexpr int kWalkThreads = 256;
+constexpr int kWalkChunk = 256;        // rows a warp claims per work-counter fetch
+
+__host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // float4 per candidate pair
+
+// FFMA2 with a scalar operand broadcast to both lanes: r = (a*b.x + c.x, a*b.y + c.y)
+__device__ __forceinline__ float2 fma2s(float a, float2 b, float2 c)
+{
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc, rr;\n\t"
+        "mov.b64 ra, {%2, %2};\n\tmov.b64 rb, {%3, %4};\n\tmov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 rr, ra, rb, rc;\n\tmov.b64 {%0, %1}, rr;\n\t}"
+        : "=f"(r.x), "=f"(r.y) : "f"(a), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+
+// squared distances to the candidate pair (j, j+1) in the centred expansion form:
+// (q_j, q_j+1) = (xx + cc_j, xx + cc_j+1) + sum_e x'_e (m_j[e], m_j+1[e]),  m = -2 c'
+// v: the pair's DP/2 float4 (coordinates interleaved by candidate); one FFMA2 per coordinate
+template <int DP>
+__device__ __forceinline__ float2 q_pair(const float (&xc)[DP], float xx, float2 cc, const float4 (&v)[DP / 2])
+{
+    float2 s = make_float2(xx + cc.x, xx + cc.y);
+#pragma unroll
+    for (int e = 0; e < DP / 2; ++e) {
+        s = fma2s(xc[2 * e], make_float2(v[e].x, v[e].y), s);
+        s = fma2s(xc[2 * e + 1], make_float2(v[e].z, v[e].w), s);
+    }
+    return s;
+}
+
+// #{j < M : h[j] < T}, M a power of two, h ascending with NaN padding: fixed-step lower bound
+template <typename P>
+__device__ __forceinline__ int count_below_pow2(P h, int M, float T)
+{
+    int base = 0;
+    for (int half = M >> 1; half >= 1; half >>= 1)
+        base = h[base + half - 1] < T ? base + half : base;
+    return base + (h[base] < T ? 1 : 0);
+}
+
+// #{j < m : h[j] < T} for ascending h (NaN padding never compares below)
+__device__ __forceinline__ int count_below_f(const float *__restrict__ h, int m, float T)
+{
+    int lo = 0, hi = m;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (h[mid] < T) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// fp64 delta reduction of a row that moved from a to b: S[b] += x, S[a] -= x (counts +-1)
+template <int DP>
+__device__ __forceinline__ void move_delta(double *acc, int d, int a, int b, const float (&x)[DP])
+{
+    double *ra = acc + (int64_t)a * (DP + 1), *rb = acc + (int64_t)b * (DP + 1);
+#pragma unroll
+    for (int j = 0; j < DP; ++j)
+        if (j < d) {
+            const double v = (double)x[j];
+            atomicAdd(rb + j, v);
+            atomicAdd(ra + j, -v);
+        }
+    atomicAdd(rb + DP, 1.0);
+    atomicAdd(ra + DP, -1.0);
+}
+
+// One lane = R rows (rows r0 + lane + 32 i); the warp walks its cluster A's candidate rows once
+// for all 32 R rows, so each broadcast load serves R rows per lane.
+template <int DP, bool CSMEM, int R>
+__global__ void __launch_bounds__(kWalkThreads)
+k_walk(AssignParams p)
+{
+    extern __shared__ __align__(16) float smem[];
+    const int k = p.k;
+    float *sC = smem;                               // k*DP (CSMEM)
+    float *sF = smem + (CSMEM ? k * DP : 0);        // k
+    float *sS = sF + k;                             // k
+    float *sH = sS + k;                             // k x whs H rows (p.wh_smem)
+    if (CSMEM) {
+        const float4 *src = reinterpret_cast<const float4 *>(p.Cneg);
+        float4 *dst = reinterpret_cast<float4 *>(sC);
+        for (int i = threadIdx.x; i < k * DP / 4; i += blockDim.x) dst[i] = src[i];
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x) { sF[i] = p.f[i]; sS[i] = p.s[i]; }
+    if (p.wh_smem)
+        for (int i = threadIdx.x; i < k * p.whs; i += blockDim.x) sH[i] = p.WH[i];
+    __syncthreads();
+    CRow<CSMEM> Cn;
+    if constexpr (CSMEM) {
+        uint32_t b = (uint32_t)__cvta_generic_to_shared(sC);
+        asm volatile("mov.u32 %0, %0;" : "+r"(b));
+        Cn.base = b;
+    } else {
+        Cn.base = p.Cneg;
+    }
+    double *acc = p.acc + (int64_t)(blockIdx.x % p.nslab) * k * (DP + 1);
+    const float eps = *p.eps;
+    const int lane = threadIdx.x & 31;
+    const int64_t n = p.n;
+    const int kp = p.wpad;                          // candidate rows per cluster block
+    const int kcols = k - 1;
+    const int ib = p.wbits;                         // key index bits
+    const uint32_t kmask = ~((1u << ib) - 1u);
+    const float qtrunc = 1.f + __uint_as_float((uint32_t)(127 - 23 + ib) << 23) * 1.0001f;   // 1 + 2^(ib-23)
+    // expansion-form error: |q~ - |x'-c'|^2| <= kappa (xx + cmax)
+    const float kappa = 2.f * (2.f * DP + 20.f) * 5.9604645e-8f;
+    constexpr int kRows = 32 * R;                   // rows per warp batch
+
+    unsigned long long c_changed = 0, c_dists = 0, c_clause1 = 0, c_refined = 0, c_fb = 0;
+    unsigned long long steps = 0;
+
+    constexpr int kBatches = kWalkChunk / kRows;
+    auto claim = [&]() -> int64_t {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(p.work, 1);
+        return (int64_t)__shfl_sync(kFull, c, 0) * kWalkChunk;
+    };
+    int64_t chunk_row = claim(), ahead_row = claim();
+    int bt = 0;
+    float nx[R][DP];
+    int na[R];
+    float nu[R];
+    auto load = [&](int64_t r0) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int64_t row = r0 + 32 * i + lane;
+            const bool v = row < n;
+            const float4 *xr = reinterpret_cast<const float4 *>(p.X + (v ? row : 0) * DP);
+#pragma unroll
+            for (int j = 0; j < DP / 4; ++j) {
+                float4 t = v ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                nx[i][4 * j] = t.x; nx[i][4 * j + 1] = t.y; nx[i][4 * j + 2] = t.z; nx[i][4 * j + 3] = t.w;
+            }
+            na[i] = v ? __ldg(p.a + row) : 0;
+            nu[i] = v ? __ldg(p.u + row) : 0.f;
+        }
+    };
+    load(chunk_row);
+
+    while (chunk_row < n) {
+        const int64_t row0 = chunk_row + bt * kRows;
+        float x[R][DP];
+        int aold[R];
+        float uu[R];
+        bool valid[R], active[R];
+        unsigned amask = 0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+#pragma unroll
+            for (int j = 0; j < DP; ++j) x[i][j] = nx[i][j];
+            aold[i] = na[i];
+            const int64_t row = row0 + 32 * i + lane;
+            valid[i] = row < n;
+            uu[i] = valid[i] ? __fadd_ru(nu[i], sF[aold[i]]) : 0.f;          // u += f(a)
+            const bool c1 = valid[i] && uu[i] <= sS[aold[i]];                  // clause 1
+            active[i] = valid[i] && !c1;
+            c_clause1 += c1;
+            amask |= __ballot_sync(kFull, active[i]) ? (1u << i) : 0u;
+        }
+        if (++bt == kBatches || chunk_row + bt * kRows >= n) {
+            bt = 0;
+            chunk_row = ahead_row;
+            ahead_row = chunk_row < n ? claim() : ahead_row;
+        }
+        if (chunk_row < n) load(chunk_row + bt * kRows);
+
+        int anew[R];
+        float unew[R], ut[R];
+        bool defer[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) { anew[i] = aold[i]; unew[i] = uu[i]; ut[i] = 0.f; defer[i] = false; }
+        if (amask) {
+            // warp cluster A: the middle row's if active, else the first active row's
+            const int mid = R == 1 ? 16 : 0;            // R = 2: lane 0 of the second half
+            const unsigned m_mid = __ballot_sync(kFull, active[R - 1]);
+            int A;
+            if ((m_mid >> mid) & 1u) A = __shfl_sync(kFull, aold[R - 1], mid);
+            else {
+                const unsigned m0 = __ballot_sync(kFull, active[0]);
+                A = m0 ? __shfl_sync(kFull, aold[0], __ffs(m0) - 1) : __shfl_sync(kFull, aold[R - 1], __ffs(m_mid) - 1);
+            }
+            float4 cA[DP / 4];
+#pragma unroll
+            for (int j = 0; j < DP / 4; ++j) cA[j] = Cn.ld(A, DP, 4 * j);
+            float xc[R][DP], xx[R], lo[R], T[R];
+            int pl[R];
+            bool misfit[R];
+            int pm = 0;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                // x' = x - C^[A] (direct form's arithmetic), xx = |x'|^2
+                float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < DP; j += 4) {
+                    const float4 c = cA[j / 4];
+                    const float2 t0 = add2(make_float2(x[i][j], x[i][j + 1]), make_float2(c.x, c.y));
+                    const float2 t1 = add2(make_float2(x[i][j + 2], x[i][j + 3]), make_float2(c.z, c.w));
+                    xc[i][j] = t0.x; xc[i][j + 1] = t0.y; xc[i][j + 2] = t1.x; xc[i][j + 3] = t1.y;
+                    a0 = fma2(t0, t0, a0);
+                    a1 = fma2(t1, t1, a1);
+                }
+                const float2 s2 = add2(a0, a1);
+                xx[i] = s2.x + s2.y;
+                misfit[i] = active[i] && aold[i] != A;
+                lo[i] = 0.f; T[i] = 0.f; pl[i] = 0;
+                if (active[i]) {
+                    if (!misfit[i]) {
+                        ut[i] = upper_d(xx[i], p.g_up, eps);
+                        lo[i] = lower_d(xx[i], p.g_dn, eps);
+                        T[i] = ut[i];
+                    } else {
+                        const float qo = dist2<DP, CSMEM>(x[i], Cn, aold[i]);
+                        ut[i] = upper_d(qo, p.g_up, eps);
+                        lo[i] = lower_d(qo, p.g_dn, eps);
+                        T[i] = __fmul_ru(__fadd_ru(ut[i], upper_d(xx[i], p.g_up, eps)), 0.5f);
+                    }
+                    pl[i] = p.wh_smem ? count_below_pow2(sH + A * p.whs, p.whs, T[i])
+                                      : count_below_pow2(p.WH + (int64_t)A * p.whs, p.whs, T[i]);
+                }
+                pm = max(pm, pl[i]);
+            }
+            pm = __reduce_max_sync(kFull, pm);
+            // the walk: candidates j < pm of A's list, two per step, keys (q & kmask) | j
+            const float4 *blk = p.Wblk + (int64_t)A * (kp / 2) * walk_pair_f4(DP);
+            const float2 *ccA = reinterpret_cast<const float2 *>(p.Wcc + (int64_t)A * kp);
+            int m1[R], m2[R];
+#pragma unroll
+            for (int i = 0; i < R; ++i) { m1[i] = 0x7fffffff; m2[i] = 0x7fffffff; }
+            for (int j = 0; j < pm; j += 2) {
+                float4 v[DP / 2];
+#pragma unroll
+                for (int e = 0; e < DP / 2; ++e) v[e] = __ldg(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e);
+                const float2 cc = __ldg(ccA + (j >> 1));
+#pragma unroll
+                for (int i = 0; i < R; ++i) {
+                    const float2 q = q_pair<DP>(xc[i], xx[i], cc, v);
+                    int k0, k1;
+                    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(k0) : "r"(__float_as_uint(q.x)), "r"(kmask), "r"(j));
+                    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(k1) : "r"(__float_as_uint(q.y)), "r"(kmask), "r"(j + 1));
+                    const int lo2 = min(k0, k1), hi2 = max(k0, k1);
+                    m2[i] = min(min(max(m1[i], lo2), m2[i]), hi2);
+                    m1[i] = min(m1[i], lo2);
+                }
+            }
+            steps += (unsigned long long)pm;
+            // prefix max of |c'|^2 over the evaluated rows (bounds the error of every key)
+            const float cmax = pm > 0 ? __ldg(p.Wmeta + (int64_t)A * kp + ((pm + 1) & ~1) - 1).x : 0.f;
+            const float2 *mA = p.Wmeta + (int64_t)A * kp;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                if (!active[i]) continue;
+                // rigorous decision (same procedure as the tensor-core epilogue)
+                const float E = __fmul_ru(kappa, __fadd_ru(xx[i], cmax));
+                const float epsr = __fadd_ru(eps, __fmul_ru(1.2e-7f, __fadd_ru(sqrt_up(xx[i]), sqrt_up(cmax))));
+                const float ue = __fadd_ru(ut[i], epsr);
+                const float thr = __fadd_ru(__fmul_ru(ue, ue), E);
+                bool fallback = false;
+                if (!misfit[i] && (m1[i] == 0x7fffffff || __int_as_float(m1[i] & kmask) > thr)) {
+                    unew[i] = ut[i];                             // stays (common case)
+                } else {
+                    auto U_of = [&](int key) {
+                        const float v = fmaxf(__int_as_float(key & kmask), 0.f);
+                        return __fadd_ru(sqrt_up(__fadd_ru(__fmul_ru(v, qtrunc), E)), epsr);
+                    };
+                    auto L_of = [&](int key) {
+                        if (key == 0x7fffffff) return INFINITY;
+                        const float v = __int_as_float(key & kmask);
+                        return fmaxf(0.f, __fsub_rd(sqrt_dn(fmaxf(__fsub_rd(v, E), 0.f)), epsr));
+                    };
+                    const int cc1 = m1[i] != 0x7fffffff ? __float_as_int(__ldg(&mA[m1[i] & ~kmask].y)) : -1;
+                    const int cc2 = m2[i] != 0x7fffffff ? __float_as_int(__ldg(&mA[m2[i] & ~kmask].y)) : -1;
+                    float Uo = ut[i], Lo = lo[i], Ui = INFINITY, Li = INFINITY, Lother = INFINITY;
+                    int ci = -1;
+                    if (cc1 == aold[i]) {      // (misfit) own cluster is the best candidate: merge
+                        Uo = fminf(Uo, U_of(m1[i])); Lo = fmaxf(Lo, L_of(m1[i]));
+                        ci = cc2;
+                        if (ci >= 0) { Ui = U_of(m2[i]); Li = L_of(m2[i]); Lother = -1.f; }   // third unknown
+                    } else {
+                        ci = cc1;
+                        if (ci >= 0) { Ui = U_of(m1[i]); Li = L_of(m1[i]); }
+                        Lother = L_of(m2[i]);
+                    }
+                    float UA = INFINITY, LA = INFINITY;
+                    if (misfit[i]) { UA = upper_d(xx[i], p.g_up, eps); LA = lower_d(xx[i], p.g_dn, eps); }
+                    if (Uo < fminf(Li, LA)) {
+                        unew[i] = Uo;
+                    } else if (misfit[i] && UA < fminf(Lo, Li)) {
+                        anew[i] = A; unew[i] = UA;
+                    } else if (ci >= 0 && Ui < fminf(fminf(Lo, LA), Lother)) {
+                        anew[i] = ci; unew[i] = Ui;
+                    } else {
+                        fallback = true;
+                    }
+                }
+                if (fallback) {
+                    ++c_fb;
+                    const uint64_t *nl = p.NL + (int64_t)aold[i] * p.ks;
+                    float bq = dist2<DP, CSMEM>(x[i], Cn, aold[i]), q2 = INFINITY;
+                    int bc = aold[i];
+                    for (int j = 0; j < kcols; ++j) {
+                        const uint64_t key = __ldg(nl + j);
+                        if (!(key_h(key) < ut[i])) break;
+                        const int c = key_c(key);
+                        const float q = dist2<DP, CSMEM>(x[i], Cn, c);
+                        q2 = fminf(q2, fmaxf(q, bq));
+                        bc = q < bq ? c : bc;
+                        bq = fminf(q, bq);
+                    }
+                    const float ub = upper_d(bq, p.g_up, eps);
+                    if (q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub) {
+                        anew[i] = refine64(p.X + (row0 + 32 * i + lane) * DP, p.d, p.C64, k, aold[i], nl, ut[i], &unew[i]);
+                        ++c_refined;
+                    } else {
+                        anew[i] = bc;
+                        unew[i] = ub;
+                    }
+                }
+                // MTI distance count 1 + #{c : H[a][c] < u_t}; misfit rows: deferred
+                if (!misfit[i]) c_dists += (unsigned long long)(1 + pl[i]);
+                defer[i] = misfit[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int64_t rb = row0 + 32 * i;
+            {   // deferred counts: compacted per 32-row group: defer[rb + i], dcount[rb / 32]
+                const unsigned dm = __ballot_sync(kFull, defer[i]);
+                if (defer[i])
+                    p.defer[rb + __popc(dm & ((1u << lane) - 1u))] =
+                        ((unsigned long long)(uint32_t)aold[i] << 32) | __float_as_uint(ut[i]);
+                if (lane == 0 && rb < n) p.dcount[rb / 32] = __popc(dm);
+            }
+            if (valid[i]) {
+                p.a[rb + lane] = anew[i];
+                p.u[rb + lane] = unew[i];
+                if (anew[i] != aold[i]) {
+                    ++c_changed;
+                    move_delta<DP>(acc, p.d, aold[i], anew[i], x[i]);   // S3 as a delta
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        c_changed += __shfl_xor_sync(kFull, c_changed, o);
+        c_dists += __shfl_xor_sync(kFull, c_dists, o);
+        c_clause1 += __shfl_xor_sync(kFull, c_clause1, o);
+        c_refined += __shfl_xor_sync(kFull, c_refined, o);
+        c_fb += __shfl_xor_sync(kFull, c_fb, o);
+    }
+    if (lane == 0) {
+        if (c_changed) atomicAdd(p.counters + 0, c_changed);
+        if (c_dists) atomicAdd(p.counters + 1, c_dists);
+        if (c_clause1) atomicAdd(p.counters + 2, c_clause1);
+        if (c_refined) atomicAdd(p.counters + 3, c_refined);
+        if (steps) atomicAdd(p.counters + 4, steps);
+        if (c_fb) atomicAdd(p.counters + 5, c_fb);
+    }
+}
+
+// S1 (walk part): per cluster c (one CTA), the candidate rows of its neighbour list NL[c]:
+//   Wblk[c][j] = -2 c'_j (DP floats), c'_j = fp32(C[c_j]) - fp32(C[c]) (RN);
+//   Wcc[c][j] = |c'_j|^2 (RN, as used in q); Wmeta[c][j] = {prefix max of |c'|^2 rounded up, c_j};
+//   WH[c][j] = H[c][c_j] (fp32, rounded down).  Rows j >= k-1 are dummies: q = xx + 1e30, H NaN.
+__global__ void k_prep_walk(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int kp, int whs,
+                            float4 *Wblk, float *Wcc, float2 *Wmeta, float *WH)
+{
+    const int c = blockIdx.x;
+    const double *Cc = C + (int64_t)c * d;
+    const uint64_t *nl = NL + (int64_t)c * ks;
+    // pair P = rows (2P, 2P+1): float e of the pair block = coordinate e/2 of row 2P + (e & 1)
+    float *blk = reinterpret_cast<float *>(Wblk + (int64_t)c * (kp / 2) * (DP / 2));
+    extern __shared__ float scn[];
+    for (int j = threadIdx.x; j < kp; j += blockDim.x) {
+        const bool real = j < k - 1;
+        const int cj = real ? key_c(nl[j]) : c;
+        const double *Cj = C + (int64_t)cj * d;
+        double cn2 = 0.0;
+        float *pairp = blk + (int64_t)(j >> 1) * 2 * DP + (j & 1);
+        for (int e = 0; e < DP; ++e) {
+            const float v = (real && e < d) ? __fsub_rn((float)Cj[e], (float)Cc[e]) : 0.f;
+            cn2 += (double)v * (double)v;
+            pairp[2 * e] = -2.f * v;
+        }
+        Wcc[(int64_t)c * kp + j] = real ? (float)cn2 : 1e30f;
+        scn[j] = real ? __double2float_ru(cn2 * (1.0 + 1e-12)) : 0.f;
+        Wmeta[(int64_t)c * kp + j].y = __int_as_float(cj);
+    }
+    for (int j = threadIdx.x; j < whs; j += blockDim.x)
+        WH[(int64_t)c * whs + j] = j < k - 1 ? key_h(nl[j]) : __int_as_float(0x7fc00000);
+    __syncthreads();
+    if (threadIdx.x == 0) {                      // prefix max of |c'|^2 (rounded up)
+        float m = 0.f;
+        for (int j = 0; j < kp; ++j) { m = fmaxf(m, scn[j]); Wmeta[(int64_t)c * kp + j].x = m; }
+    }
+}
+
+cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int kp, int whs,
+                             float4 *Wblk, float *Wcc, float2 *Wmeta, float *WH, cudaStream_t st)
+{
+    k_prep_walk<<<k, 128, (size_t)kp * sizeof(float), st>>>(C, NL, k, d, DP, ks, kp, whs, Wblk, Wcc, Wmeta, WH);
+    return cudaGetLastError();
+}
+
+size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem)
+{
+    return (size_t)((csmem ? k * DP : 0) + 2 * k + (wh_smem ? k * whs : 0)) * sizeof(float);
+}
+
+// rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
+template <int DP> constexpr int walk_r() { return DP <= 16 ? 2 : 1; }
+
+template <int DP, bool CSMEM>
+static cudaError_t launch_walk_t(const AssignParams &p, int grid, cudaStream_t st)
+{
+    const size_t sm = walk_smem(DP, CSMEM, p.k, p.whs, p.wh_smem);
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_walk<DP, CSMEM, walk_r<DP>()>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+    }
+    k_walk<DP, CSMEM, walk_r<DP>()><<<grid, kWalkThreads, sm, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int DP, bool CSMEM>
+static int walk_grid_t(int k, int kp, bool whs, int num_sms)
+{
+    int per_sm = 0;
+    const size_t sm = walk_smem(DP, CSMEM, k, kp, whs);
+    if (sm > 48 * 1024)
+        cudaFuncSetAttribute(k_walk<DP, CSMEM, walk_r<DP>()>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<DP, CSMEM, walk_r<DP>()>, kWalkThreads, sm);
+    return (per_sm < 1 ? 1 : per_sm) * num_sms;
+}
+
+bool walk_supported(int DP) { return DP == 4 || DP == 8 || DP == 16 || DP == 32 || DP == 64; }
+
+cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st)
+{
+    switch (DP * 2 + (csmem ? 1 : 0)) {
+    case 8: return launch_walk_t<4, false>(p, grid, st);
+    case 9: return launch_walk_t<4, true>(p, grid, st);
+    case 16: return launch_walk_t<8, false>(p, grid, st);
+    case 17: return launch_walk_t<8, true>(p, grid, st);
+    case 32: return launch_walk_t<16, false>(p, grid, st);
+    case 33: return launch_walk_t<16, true>(p, grid, st);
+    case 64: return launch_walk_t<32, false>(p, grid, st);
+    case 65: return launch_walk_t<32, true>(p, grid, st);
+    case 128: return launch_walk_t<64, false>(p, grid, st);
+    case 129: return launch_walk_t<64, true>(p, grid, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int walk_grid(int DP, bool csmem, int k, int kp, bool whs, int num_sms)
+{
+    switch (DP * 2 + (csmem ? 1 : 0)) {
+    case 8: return walk_grid_t<4, false>(k, kp, whs, num_sms);
+    case 9: return walk_grid_t<4, true>(k, kp, whs, num_sms);
+    case 16: return walk_grid_t<8, false>(k, kp, whs, num_sms);
+    case 17: return walk_grid_t<8, true>(k, kp, whs, num_sms);
+    case 32: return walk_grid_t<16, false>(k, kp, whs, num_sms);
+    case 33: return walk_grid_t<16, true>(k, kp, whs, num_sms);
+    case 64: return walk_grid_t<32, false>(k, kp, whs, num_sms);
+    case 65: return walk_grid_t<32, true>(k, kp, whs, num_sms);
+    case 128: return walk_grid_t<64, false>(k, kp, whs, num_sms);
+    case 129: return walk_grid_t<64, true>(k, kp, whs, num_sms);
+    }
+    return num_sms;
+}
+
+}  // namespace km
