@@ -547,9 +547,10 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         c->wpad = (k + 1) & ~1;                    // k-1 neighbours + >= 1 dummy row, even
         c->wbits = 1;
         while ((1 << c->wbits) < c->wpad) ++c->wbits;
-        c->whs = 2;
+        c->whs = 16;
         while (c->whs < c->wpad) c->whs <<= 1;
-        c->wh_smem = (size_t)k * c->whs * sizeof(float) <= 64 * 1024;
+        c->wh_smem = c->whs <= 256 && (size_t)k * c->whs * sizeof(float) <= 56 * 1024 && !getenv("KM_WH_GLOBAL");
+        if (!c->wh_smem && c->whs < 256) c->whs = 256;
         KM_TRY(dalloc(&c->Wblk, (size_t)k * (c->wpad / 2) * (DP / 2)));
         KM_TRY(dalloc(&c->Wcc, (size_t)k * c->wpad));
         KM_TRY(dalloc(&c->Wmeta, (size_t)k * c->wpad));

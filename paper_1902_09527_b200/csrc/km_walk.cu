@@ -61,14 +61,20 @@ __device__ __forceinline__ float2 q_pair(const float (&xc)[DP], float xx, float2
     return s;
 }
 
-// #{j < M : h[j] < T}, M a power of two, h ascending with NaN padding: fixed-step lower bound
-template <typename P>
-__device__ __forceinline__ int count_below_pow2(P h, int M, float T)
+// #{j < NH : h[j] < T}, NH a power of two, h ascending with NaN padding: unrolled lower bound
+template <int NH, typename P>
+__device__ __forceinline__ int count_below_u(P h, float T)
 {
     int base = 0;
-    for (int half = M >> 1; half >= 1; half >>= 1)
+#pragma unroll
+    for (int half = NH >> 1; half >= 1; half >>= 1)
         base = h[base + half - 1] < T ? base + half : base;
     return base + (h[base] < T ? 1 : 0);
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
 }
 
 // #{j < m : h[j] < T} for ascending h (NaN padding never compares below)
@@ -100,8 +106,8 @@ __device__ __forceinline__ void move_delta(double *acc, int d, int a, int b, con
 
 // One lane = R rows (rows r0 + lane + 32 i); the warp walks its cluster A's candidate rows once
 // for all 32 R rows, so each broadcast load serves R rows per lane.
-template <int DP, bool CSMEM, int R>
-__global__ void __launch_bounds__(kWalkThreads)
+template <int DP, bool CSMEM, int R, int NH, bool HSMEM>
+__global__ void __launch_bounds__(kWalkThreads, 3)
 k_walk(AssignParams p)
 {
     extern __shared__ __align__(16) float smem[];
@@ -109,15 +115,18 @@ k_walk(AssignParams p)
     float *sC = smem;                               // k*DP (CSMEM)
     float *sF = smem + (CSMEM ? k * DP : 0);        // k
     float *sS = sF + k;                             // k
-    float *sH = sS + k;                             // k x whs H rows (p.wh_smem)
+    float *sH = sS + k;                             // k x NH H rows (HSMEM)
+    // per-warp staging of the next batch (cp.async): x rows, then a, then u
+    constexpr int kRowsB = 32 * R;
+    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2));
     if (CSMEM) {
         const float4 *src = reinterpret_cast<const float4 *>(p.Cneg);
         float4 *dst = reinterpret_cast<float4 *>(sC);
         for (int i = threadIdx.x; i < k * DP / 4; i += blockDim.x) dst[i] = src[i];
     }
     for (int i = threadIdx.x; i < k; i += blockDim.x) { sF[i] = p.f[i]; sS[i] = p.s[i]; }
-    if (p.wh_smem)
-        for (int i = threadIdx.x; i < k * p.whs; i += blockDim.x) sH[i] = p.WH[i];
+    if (HSMEM)
+        for (int i = threadIdx.x; i < k * NH; i += blockDim.x) sH[i] = p.WH[i];
     __syncthreads();
     CRow<CSMEM> Cn;
     if constexpr (CSMEM) {
@@ -151,28 +160,23 @@ k_walk(AssignParams p)
     };
     int64_t chunk_row = claim(), ahead_row = claim();
     int bt = 0;
-    float nx[R][DP];
-    int na[R];
-    float nu[R];
-    auto load = [&](int64_t r0) {
+    // stage rows [r0, r0 + 32 R) of X, a, u into this warp's buffer (16-B cp.async per lane)
+    auto stage = [&](int64_t r0) {
+        const float4 *xs = reinterpret_cast<const float4 *>(p.X + r0 * DP);
+        float4 *xd = reinterpret_cast<float4 *>(stg);
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const int64_t row = r0 + 32 * i + lane;
-            const bool v = row < n;
-            const float4 *xr = reinterpret_cast<const float4 *>(p.X + (v ? row : 0) * DP);
-#pragma unroll
-            for (int j = 0; j < DP / 4; ++j) {
-                float4 t = v ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-                nx[i][4 * j] = t.x; nx[i][4 * j + 1] = t.y; nx[i][4 * j + 2] = t.z; nx[i][4 * j + 3] = t.w;
-            }
-            na[i] = v ? __ldg(p.a + row) : 0;
-            nu[i] = v ? __ldg(p.u + row) : 0.f;
-        }
+        for (int c = lane; c < kRowsB * DP / 4; c += 32) cp_async16(xd + c, xs + c);
+        float *ad = stg + kRowsB * DP;
+        if (lane < kRowsB / 4) cp_async16(ad + 4 * lane, p.a + r0 + 4 * lane);
+        else if (lane < kRowsB / 2) cp_async16(ad + kRowsB + 4 * (lane - kRowsB / 4), p.u + r0 + 4 * (lane - kRowsB / 4));
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    load(chunk_row);
+    if (chunk_row < n) stage(chunk_row);
 
     while (chunk_row < n) {
         const int64_t row0 = chunk_row + bt * kRows;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
         float x[R][DP];
         int aold[R];
         float uu[R];
@@ -180,23 +184,30 @@ k_walk(AssignParams p)
         unsigned amask = 0;
 #pragma unroll
         for (int i = 0; i < R; ++i) {
+            const int r = 32 * i + lane;
 #pragma unroll
-            for (int j = 0; j < DP; ++j) x[i][j] = nx[i][j];
-            aold[i] = na[i];
-            const int64_t row = row0 + 32 * i + lane;
+            for (int j = 0; j < DP; j += 4) {
+                const float4 t = *reinterpret_cast<const float4 *>(stg + r * DP + j);
+                x[i][j] = t.x; x[i][j + 1] = t.y; x[i][j + 2] = t.z; x[i][j + 3] = t.w;
+            }
+            aold[i] = __float_as_int(stg[kRowsB * DP + r]);
+            const float uold = stg[kRowsB * DP + kRowsB + r];
+            const int64_t row = row0 + r;
             valid[i] = row < n;
-            uu[i] = valid[i] ? __fadd_ru(nu[i], sF[aold[i]]) : 0.f;          // u += f(a)
+            if (!valid[i]) aold[i] = 0;
+            uu[i] = valid[i] ? __fadd_ru(uold, sF[aold[i]]) : 0.f;          // u += f(a)
             const bool c1 = valid[i] && uu[i] <= sS[aold[i]];                  // clause 1
             active[i] = valid[i] && !c1;
             c_clause1 += c1;
             amask |= __ballot_sync(kFull, active[i]) ? (1u << i) : 0u;
         }
+        __syncwarp();
         if (++bt == kBatches || chunk_row + bt * kRows >= n) {
             bt = 0;
             chunk_row = ahead_row;
             ahead_row = chunk_row < n ? claim() : ahead_row;
         }
-        if (chunk_row < n) load(chunk_row + bt * kRows);
+        if (chunk_row < n) stage(chunk_row + bt * kRows);
 
         int anew[R];
         float unew[R], ut[R];
@@ -248,8 +259,8 @@ k_walk(AssignParams p)
                         lo[i] = lower_d(qo, p.g_dn, eps);
                         T[i] = __fmul_ru(__fadd_ru(ut[i], upper_d(xx[i], p.g_up, eps)), 0.5f);
                     }
-                    pl[i] = p.wh_smem ? count_below_pow2(sH + A * p.whs, p.whs, T[i])
-                                      : count_below_pow2(p.WH + (int64_t)A * p.whs, p.whs, T[i]);
+                    if constexpr (HSMEM) pl[i] = count_below_u<NH>(sH + A * NH, T[i]);
+                    else pl[i] = count_below_u<NH>(p.WH + (int64_t)A * NH, T[i]);
                 }
                 pm = max(pm, pl[i]);
             }
@@ -329,13 +340,22 @@ k_walk(AssignParams p)
                 if (fallback) {
                     ++c_fb;
                     const uint64_t *nl = p.NL + (int64_t)aold[i] * p.ks;
-                    float bq = dist2<DP, CSMEM>(x[i], Cn, aold[i]), q2 = INFINITY;
+                    float xr[DP];
+                    {
+                        const float4 *src = reinterpret_cast<const float4 *>(p.X + (row0 + 32 * i + lane) * DP);
+#pragma unroll
+                        for (int j = 0; j < DP / 4; ++j) {
+                            const float4 t = __ldg(src + j);
+                            xr[4 * j] = t.x; xr[4 * j + 1] = t.y; xr[4 * j + 2] = t.z; xr[4 * j + 3] = t.w;
+                        }
+                    }
+                    float bq = dist2<DP, CSMEM>(xr, Cn, aold[i]), q2 = INFINITY;
                     int bc = aold[i];
                     for (int j = 0; j < kcols; ++j) {
                         const uint64_t key = __ldg(nl + j);
                         if (!(key_h(key) < ut[i])) break;
                         const int c = key_c(key);
-                        const float q = dist2<DP, CSMEM>(x[i], Cn, c);
+                        const float q = dist2<DP, CSMEM>(xr, Cn, c);
                         q2 = fminf(q2, fmaxf(q, bq));
                         bc = q < bq ? c : bc;
                         bq = fminf(q, bq);
@@ -369,7 +389,14 @@ k_walk(AssignParams p)
                 p.u[rb + lane] = unew[i];
                 if (anew[i] != aold[i]) {
                     ++c_changed;
-                    move_delta<DP>(acc, p.d, aold[i], anew[i], x[i]);   // S3 as a delta
+                    float xr[DP];
+                    const float4 *src = reinterpret_cast<const float4 *>(p.X + (rb + lane) * DP);
+#pragma unroll
+                    for (int j = 0; j < DP / 4; ++j) {
+                        const float4 t = __ldg(src + j);
+                        xr[4 * j] = t.x; xr[4 * j + 1] = t.y; xr[4 * j + 2] = t.z; xr[4 * j + 3] = t.w;
+                    }
+                    move_delta<DP>(acc, p.d, aold[i], anew[i], xr);     // S3 as a delta
                 }
             }
         }
@@ -438,69 +465,81 @@ cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, 
 
 size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem)
 {
-    return (size_t)((csmem ? k * DP : 0) + 2 * k + (wh_smem ? k * whs : 0)) * sizeof(float);
+    const int R = DP <= 16 ? 2 : 1;
+    return (size_t)((csmem ? k * DP : 0) + 2 * k + (wh_smem ? k * whs : 0)) * sizeof(float) +
+           (size_t)(kWalkThreads / 32) * 32 * R * (DP + 2) * sizeof(float);
 }
 
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
 template <int DP> constexpr int walk_r() { return DP <= 16 ? 2 : 1; }
 
-template <int DP, bool CSMEM>
-static cudaError_t launch_walk_t(const AssignParams &p, int grid, cudaStream_t st)
-{
-    const size_t sm = walk_smem(DP, CSMEM, p.k, p.whs, p.wh_smem);
-    if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_walk<DP, CSMEM, walk_r<DP>()>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-    }
-    k_walk<DP, CSMEM, walk_r<DP>()><<<grid, kWalkThreads, sm, st>>>(p);
-    return cudaGetLastError();
-}
+typedef void (*walk_kernel_t)(AssignParams);
 
 template <int DP, bool CSMEM>
-static int walk_grid_t(int k, int kp, bool whs, int num_sms)
+static walk_kernel_t walk_pick(int whs, bool hs)
 {
-    int per_sm = 0;
-    const size_t sm = walk_smem(DP, CSMEM, k, kp, whs);
-    if (sm > 48 * 1024)
-        cudaFuncSetAttribute(k_walk<DP, CSMEM, walk_r<DP>()>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<DP, CSMEM, walk_r<DP>()>, kWalkThreads, sm);
-    return (per_sm < 1 ? 1 : per_sm) * num_sms;
+    constexpr int R = walk_r<DP>();
+    if (hs) {
+        switch (whs) {
+        case 2: case 4: case 8: case 16: return k_walk<DP, CSMEM, R, 16, true>;
+        case 32: return k_walk<DP, CSMEM, R, 32, true>;
+        case 64: return k_walk<DP, CSMEM, R, 64, true>;
+        case 128: return k_walk<DP, CSMEM, R, 128, true>;
+        case 256: return k_walk<DP, CSMEM, R, 256, true>;
+        }
+    } else {
+        switch (whs) {
+        case 256: return k_walk<DP, CSMEM, R, 256, false>;
+        case 512: return k_walk<DP, CSMEM, R, 512, false>;
+        case 1024: return k_walk<DP, CSMEM, R, 1024, false>;
+        case 2048: return k_walk<DP, CSMEM, R, 2048, false>;
+        case 4096: return k_walk<DP, CSMEM, R, 4096, false>;
+        }
+    }
+    return nullptr;
+}
+
+static walk_kernel_t walk_kernel(int DP, bool csmem, int whs, bool hs)
+{
+    switch (DP * 2 + (csmem ? 1 : 0)) {
+    case 8: return walk_pick<4, false>(whs, hs);
+    case 9: return walk_pick<4, true>(whs, hs);
+    case 16: return walk_pick<8, false>(whs, hs);
+    case 17: return walk_pick<8, true>(whs, hs);
+    case 32: return walk_pick<16, false>(whs, hs);
+    case 33: return walk_pick<16, true>(whs, hs);
+    case 64: return walk_pick<32, false>(whs, hs);
+    case 65: return walk_pick<32, true>(whs, hs);
+    case 128: return walk_pick<64, false>(whs, hs);
+    case 129: return walk_pick<64, true>(whs, hs);
+    }
+    return nullptr;
 }
 
 bool walk_supported(int DP) { return DP == 4 || DP == 8 || DP == 16 || DP == 32 || DP == 64; }
 
 cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st)
 {
-    switch (DP * 2 + (csmem ? 1 : 0)) {
-    case 8: return launch_walk_t<4, false>(p, grid, st);
-    case 9: return launch_walk_t<4, true>(p, grid, st);
-    case 16: return launch_walk_t<8, false>(p, grid, st);
-    case 17: return launch_walk_t<8, true>(p, grid, st);
-    case 32: return launch_walk_t<16, false>(p, grid, st);
-    case 33: return launch_walk_t<16, true>(p, grid, st);
-    case 64: return launch_walk_t<32, false>(p, grid, st);
-    case 65: return launch_walk_t<32, true>(p, grid, st);
-    case 128: return launch_walk_t<64, false>(p, grid, st);
-    case 129: return launch_walk_t<64, true>(p, grid, st);
+    walk_kernel_t kern = walk_kernel(DP, csmem, p.whs, p.wh_smem != 0);
+    if (!kern) return cudaErrorInvalidValue;
+    const size_t sm = walk_smem(DP, csmem, p.k, p.whs, p.wh_smem != 0);
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
     }
-    return cudaErrorInvalidValue;
+    kern<<<grid, kWalkThreads, sm, st>>>(p);
+    return cudaGetLastError();
 }
 
-int walk_grid(int DP, bool csmem, int k, int kp, bool whs, int num_sms)
+int walk_grid(int DP, bool csmem, int k, int whs, bool hs, int num_sms)
 {
-    switch (DP * 2 + (csmem ? 1 : 0)) {
-    case 8: return walk_grid_t<4, false>(k, kp, whs, num_sms);
-    case 9: return walk_grid_t<4, true>(k, kp, whs, num_sms);
-    case 16: return walk_grid_t<8, false>(k, kp, whs, num_sms);
-    case 17: return walk_grid_t<8, true>(k, kp, whs, num_sms);
-    case 32: return walk_grid_t<16, false>(k, kp, whs, num_sms);
-    case 33: return walk_grid_t<16, true>(k, kp, whs, num_sms);
-    case 64: return walk_grid_t<32, false>(k, kp, whs, num_sms);
-    case 65: return walk_grid_t<32, true>(k, kp, whs, num_sms);
-    case 128: return walk_grid_t<64, false>(k, kp, whs, num_sms);
-    case 129: return walk_grid_t<64, true>(k, kp, whs, num_sms);
-    }
-    return num_sms;
+    walk_kernel_t kern = walk_kernel(DP, csmem, whs, hs);
+    if (!kern) return num_sms;
+    const size_t sm = walk_smem(DP, csmem, k, whs, hs);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWalkThreads, sm);
+    return (per_sm < 1 ? 1 : per_sm) * num_sms;
 }
 
 }  // namespace km
