@@ -113,9 +113,10 @@ k_walk(AssignParams p)
     extern __shared__ __align__(16) float smem[];
     const int k = p.k;
     float *sC = smem;                               // k*DP (CSMEM)
+    const int k4 = (k + 3) & ~3;                   // sections stay 16-B aligned
     float *sF = smem + (CSMEM ? k * DP : 0);        // k
-    float *sS = sF + k;                             // k
-    float *sH = sS + k;                             // k x NH H rows (HSMEM)
+    float *sS = sF + k4;                            // k
+    float *sH = sS + k4;                            // k x NH H rows (HSMEM)
     // per-warp staging of the next batch (cp.async): x rows, then a, then u
     constexpr int kRowsB = 32 * R;
     float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2));
@@ -466,7 +467,8 @@ cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, 
 size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem)
 {
     const int R = DP <= 16 ? 2 : 1;
-    return (size_t)((csmem ? k * DP : 0) + 2 * k + (wh_smem ? k * whs : 0)) * sizeof(float) +
+    const int k4 = (k + 3) & ~3;
+    return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
            (size_t)(kWalkThreads / 32) * 32 * R * (DP + 2) * sizeof(float);
 }
 
