@@ -111,11 +111,14 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def traffic_from_profile(cfg: str, prune: str):
+def traffic_from_profile(cfg: str, prune: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel`` from the committed
+    ncu capture summary (profiles/traffic_<cfg>_<prune>.json), or None if it is for another kernel."""
     p = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{prune}.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            j = json.load(open(p))
+            return j.get("dram_bytes_per_launch") if j.get("kernel_name", "") == kernel else None
         except Exception:
             return None
     return None
@@ -233,6 +236,7 @@ def run_ours(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1)
     ms_max = max_over_ranks(ms)
     launches = km.launch_count - launches0
+    engine = km.engine
     stats = km.stats()
     timed = stats[args.warmup:args.warmup + args.steps]
     assign_ms = [s["ms_assign"] for s in timed]
@@ -263,8 +267,8 @@ def run_ours(args, rank, world, local_rank):
         "dists_computed_per_s": dists_computed / (ms_max * 1e-3),
         "hbm_gbs_step": iter_bytes * iters_per_s / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_from_profile(args.config, args.prune),
-                     "kernel": "k_assign<MTI_REDUCE>" if args.prune == "mti" else "k_assign<DENSE_REDUCE>",
+                     "frac": achieved / peak, "traffic": traffic_from_profile(args.config, args.prune, engine),
+                     "kernel": engine,
                      "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": avg_assign,
                      "peak_source": peak_src},
         "gpu_launches": launches,

@@ -152,6 +152,11 @@ km_status kmeans_get_stats(km_ctx *ctx, km_iter_stats *out, int32_t cap, int32_t
 /* Number of kernel launches this context has issued so far (for launch accounting). */
 int64_t kmeans_launch_count(const km_ctx *ctx);
 
+/* Name of the kernel that runs the MTI assignment pass (S2+S3) of this context:
+ * "k_walk" (CUDA-core walk engine), "k_mti_tc" (tcgen05 engine), "k_assign" (direct-form lane
+ * walk, legacy) or "k_assign_dense" (KM_PRUNE_NONE).  Static string; NULL ctx -> "". */
+const char *kmeans_engine(const km_ctx *ctx);
+
 /* Release all device memory, the internal stream (if created) and the NCCL communicator. */
 void kmeans_destroy(km_ctx *ctx);
 

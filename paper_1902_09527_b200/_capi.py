@@ -52,6 +52,7 @@ SIGNATURES = {
     "kmeans_get_stats": (ct.c_int32, [ct.c_void_p, ct.POINTER(KmIterStats), ct.c_int32,
                                       ct.POINTER(ct.c_int32)]),
     "kmeans_launch_count": (ct.c_int64, [ct.c_void_p]),
+    "kmeans_engine": (ct.c_char_p, [ct.c_void_p]),
     "kmeans_destroy": (None, [ct.c_void_p]),
     "kmeans_last_error": (ct.c_char_p, []),
     "kmeans_version": (ct.c_char_p, []),

@@ -257,9 +257,11 @@ km_status launch_assign(km_ctx *c, int mode, int work_slot)
     if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
         if (c->use_tc) KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
         else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->st));
-        KM_CUDA(km::launch_mti_count(c->defer, c->dcount, c->n_alloc / 128, c->counters, c->NL, c->ks, c->k,
-                                     c->num_sms, c->st));
-        c->launches += 1;
+        if (c->use_tc || !c->wh_smem) {   // deferred distance counts (misfit rows)
+            KM_CUDA(km::launch_mti_count(c->defer, c->dcount, c->n_alloc / 128, c->counters, c->NL, c->ks, c->k,
+                                         c->num_sms, c->st));
+            c->launches += 1;
+        }
     }
     else
         KM_CUDA(km::launch_assign(mode, c->DP, c->csmem, p, c->grid_assign[mode], c->st));
@@ -733,6 +735,13 @@ km_status kmeans_get_stats(km_ctx *c, km_iter_stats *out, int32_t cap, int32_t *
 }
 
 int64_t kmeans_launch_count(const km_ctx *c) { return c ? c->launches : 0; }
+
+const char *kmeans_engine(const km_ctx *c)
+{
+    if (!c) return "";
+    if (c->prune != KM_PRUNE_MTI) return "k_assign_dense";
+    return c->use_tc ? "k_mti_tc" : (c->use_walk ? "k_walk" : "k_assign");
+}
 
 void kmeans_destroy(km_ctx *c)
 {

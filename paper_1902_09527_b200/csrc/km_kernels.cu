@@ -515,6 +515,8 @@ __global__ void k_scan_buckets(SortParams p)    // one CTA
     }
 }
 
+// Rows of a warp that go to the same bucket take consecutive slots (one smem atomic per bucket
+// group, __match_any_sync), so a nearly sorted input is written back in coalesced runs.
 template <int DP>
 __global__ void k_scatter(SortParams p)
 {
@@ -522,12 +524,21 @@ __global__ void k_scatter(SortParams p)
     for (int b = threadIdx.x; b < p.NB; b += blockDim.x)
         cur[b] = p.base[b] + p.hist[(int64_t)b * p.ntiles + blockIdx.x];
     __syncthreads();
+    const int lane = threadIdx.x & 31;
     const int64_t r0 = (int64_t)blockIdx.x * p.tile_rows;
     int64_t r1 = r0 + p.tile_rows;
     if (r1 > p.n) r1 = p.n;
-    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        const uint32_t b = p.keys[r];
-        const int64_t dst = atomicAdd(&cur[b], 1u);
+    for (int64_t rb = r0 + (threadIdx.x & ~31); rb < r1; rb += blockDim.x) {
+        const int64_t r = rb + lane;
+        const bool v = r < r1;
+        const uint32_t b = v ? p.keys[r] : 0xffffffffu;
+        const unsigned grp = __match_any_sync(kFull, b);
+        const int leader = __ffs(grp) - 1;
+        uint32_t base = 0;
+        if (v && lane == leader) base = atomicAdd(&cur[b], (uint32_t)__popc(grp));
+        base = __shfl_sync(kFull, base, leader);
+        if (!v) continue;
+        const int64_t dst = base + __popc(grp & ((1u << lane) - 1u));
         const float4 *src = reinterpret_cast<const float4 *>(p.X + r * DP);
         float4 *dx = reinterpret_cast<float4 *>(p.X2 + dst * DP);
 #pragma unroll

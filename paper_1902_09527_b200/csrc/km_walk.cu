@@ -371,14 +371,19 @@ k_walk(AssignParams p)
                     }
                 }
                 // MTI distance count 1 + #{c : H[a][c] < u_t}; misfit rows: deferred
-                if (!misfit[i]) c_dists += (unsigned long long)(1 + pl[i]);
-                defer[i] = misfit[i];
+                if (!misfit[i]) {
+                    c_dists += (unsigned long long)(1 + pl[i]);
+                } else if constexpr (HSMEM) {      // own list's H row is in shared memory
+                    c_dists += (unsigned long long)(1 + count_below_u<NH>(sH + aold[i] * NH, ut[i]));
+                } else {
+                    defer[i] = true;                 // counted by k_mti_count
+                }
             }
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const int64_t rb = row0 + 32 * i;
-            {   // deferred counts: compacted per 32-row group: defer[rb + i], dcount[rb / 32]
+            if constexpr (!HSMEM) {   // deferred counts: per 32-row group: defer[rb + i], dcount[rb / 32]
                 const unsigned dm = __ballot_sync(kFull, defer[i]);
                 if (defer[i])
                     p.defer[rb + __popc(dm & ((1u << lane) - 1u))] =

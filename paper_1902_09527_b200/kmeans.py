@@ -131,6 +131,11 @@ class KMeans:
     def launch_count(self) -> int:
         return int(C.lib().kmeans_launch_count(self._h))
 
+    @property
+    def engine(self) -> str:
+        """Kernel of the MTI assignment pass ("k_walk", "k_mti_tc", "k_assign", "k_assign_dense")."""
+        return C.lib().kmeans_engine(self._h).decode()
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             C.lib().kmeans_destroy(self._h)

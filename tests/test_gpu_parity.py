@@ -248,3 +248,38 @@ def test_bound_soundness_sampled():
         a_o, d1, _ = oracle.assign_brute(X, Cused)
         assert np.array_equal(a, a_o)
     km.close()
+
+
+# ---- BASELINE full size, bench launch configuration ----------------------------------------
+def test_c3_full_size_free_running_and_sampled():
+    """C3 at its full BASELINE size (n = 65,608,366, d = 8, k = 100) through the same engine and
+    launch configuration bench.py times: free-running strict parity with the oracle for the first
+    iterations, then single-step checks of sampled rows (fp64 brute-force argmin against the
+    centroids the pass used) and of the centroids (oracle means of the GPU's assignments)."""
+    X, idx, spec = make_config("c3")
+    assert X.shape == (65_608_366, 8)
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, 3, 0, "mti")
+    Xd = torch.from_numpy(X).cuda()
+    km = KMeans(Xd, C0, prune="mti")
+    for _ in range(3):
+        km.iterate()
+    g = dict(iterations=3, a=km.assignments(), C=km.centroids(), sse=km.sse(), stats=km.stats())
+    assert np.array_equal(g["a"], r.a), int((g["a"] != r.a).sum())
+    assert centroid_rel_err(g["C"], r.C).max() <= 1e-12
+    assert [s["changed"] for s in g["stats"]] == r.changed.tolist()
+    # later iterations: single-step checks on a sample
+    rng = np.random.default_rng(7)
+    sample = np.sort(rng.choice(X.shape[0], 400_000, replace=False))
+    for _ in range(5):
+        Cused = km.centroids()
+        km.iterate()
+    a = km.assignments()
+    a_o, d1, d2 = oracle.assign_brute(X[sample], Cused)
+    ok = ~near_tie_mask(d1, d2)
+    assert np.array_equal(a[sample][ok], a_o[ok])
+    assert int((a[sample] != a_o).sum()) == 0
+    sums, counts = oracle.cluster_sums(X, a, 100)
+    C_means, _ = oracle.update(sums, counts, Cused)
+    assert centroid_rel_err(km.centroids(), C_means).max() <= 1e-12
+    km.close()
