@@ -425,6 +425,16 @@ cudaError_t launch_update(const double *acc, double *S, int delta, double *C, do
 // Re-bucketing (counting sort by bucket = a * Q + prefix class).  The prefix length
 // p = #{c' : H[a][c'] < u} is the number of candidates the point would evaluate; rows of a
 // bucket therefore have similar walk lengths, which keeps warp lanes busy.
+__device__ __forceinline__ uint32_t bucket_class(int a, int lo, int k, int Q)
+{
+    int q = 0;
+    if (lo > 0) {
+        int64_t t = 1 + (int64_t)(lo - 1) * (Q - 1) / (k > 1 ? k - 1 : 1);
+        q = (int)(t < Q - 1 ? t : Q - 1);
+    }
+    return (uint32_t)a * Q + q;
+}
+
 __device__ __forceinline__ uint32_t bucket_of(int a, float u, const uint64_t *NL, int k, int ks, int Q)
 {
     if (Q == 1) return (uint32_t)a;
@@ -434,24 +444,44 @@ __device__ __forceinline__ uint32_t bucket_of(int a, float u, const uint64_t *NL
         int mid = (lo + hi) >> 1;
         if (key_h(__ldg(nl + mid)) < u) lo = mid + 1; else hi = mid;
     }
-    int q = 0;
-    if (lo > 0) {
-        int64_t t = 1 + (int64_t)(lo - 1) * (Q - 1) / (k > 1 ? k - 1 : 1);
-        q = (int)(t < Q - 1 ? t : Q - 1);
-    }
-    return (uint32_t)a * Q + q;
+    return bucket_class(a, lo, k, Q);
 }
+
+// Bucket keys + per-tile histograms.  For k <= kSortSmemK the H rows of all clusters are staged
+// in shared memory, so the prefix search costs no dependent global loads.
+constexpr int kSortSmemK = 128;
 
 __global__ void k_sort_keys(SortParams p)
 {
     extern __shared__ uint32_t sh[];
+    const int k = p.k;
+    const bool hs = p.Q > 1 && k <= kSortSmemK;
+    float *sH = reinterpret_cast<float *>(sh + p.NB);   // k x k (row c: H[c][.] ascending, NaN pad)
     for (int b = threadIdx.x; b < p.NB; b += blockDim.x) sh[b] = 0;
+    if (hs)
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+            const int c = i / k, j = i % k;
+            sH[i] = j < k - 1 ? key_h(p.NL[(int64_t)c * p.ks + j]) : __int_as_float(0x7fc00000);
+        }
     __syncthreads();
     const int64_t r0 = (int64_t)blockIdx.x * p.tile_rows;
     int64_t r1 = r0 + p.tile_rows;
     if (r1 > p.n) r1 = p.n;
     for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        uint32_t b = bucket_of(p.a[r], p.u[r], p.NL, p.k, p.ks, p.Q);
+        const int a = p.a[r];
+        const float u = p.u[r];
+        uint32_t b;
+        if (hs) {
+            const float *h = sH + a * k;
+            int lo = 0, hi = k - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (h[mid] < u) lo = mid + 1; else hi = mid;
+            }
+            b = bucket_class(a, lo, k, p.Q);
+        } else {
+            b = bucket_of(a, u, p.NL, k, p.ks, p.Q);
+        }
         p.keys[r] = b;
         atomicAdd(&sh[b], 1u);
     }
@@ -517,9 +547,13 @@ __global__ void k_scan_buckets(SortParams p)    // one CTA
 
 // Rows of a warp that go to the same bucket take consecutive slots (one smem atomic per bucket
 // group, __match_any_sync), so a nearly sorted input is written back in coalesced runs.
+// Rows of a warp that go to the same bucket take consecutive slots (one smem atomic per bucket
+// group, __match_any_sync), so a nearly sorted input is written back in coalesced runs.  Each
+// warp handles G groups of 32 rows per step with all loads issued first (memory parallelism).
 template <int DP>
-__global__ void k_scatter(SortParams p)
+__global__ void __launch_bounds__(512) k_scatter(SortParams p)
 {
+    constexpr int G = DP <= 16 ? 4 : 2;
     extern __shared__ uint32_t cur[];
     for (int b = threadIdx.x; b < p.NB; b += blockDim.x)
         cur[b] = p.base[b] + p.hist[(int64_t)b * p.ntiles + blockIdx.x];
@@ -528,31 +562,52 @@ __global__ void k_scatter(SortParams p)
     const int64_t r0 = (int64_t)blockIdx.x * p.tile_rows;
     int64_t r1 = r0 + p.tile_rows;
     if (r1 > p.n) r1 = p.n;
-    for (int64_t rb = r0 + (threadIdx.x & ~31); rb < r1; rb += blockDim.x) {
-        const int64_t r = rb + lane;
-        const bool v = r < r1;
-        const uint32_t b = v ? p.keys[r] : 0xffffffffu;
-        const unsigned grp = __match_any_sync(kFull, b);
-        const int leader = __ffs(grp) - 1;
-        uint32_t base = 0;
-        if (v && lane == leader) base = atomicAdd(&cur[b], (uint32_t)__popc(grp));
-        base = __shfl_sync(kFull, base, leader);
-        if (!v) continue;
-        const int64_t dst = base + __popc(grp & ((1u << lane) - 1u));
-        const float4 *src = reinterpret_cast<const float4 *>(p.X + r * DP);
-        float4 *dx = reinterpret_cast<float4 *>(p.X2 + dst * DP);
+    for (int64_t rb = r0 + (threadIdx.x & ~31) * G; rb < r1; rb += (int64_t)blockDim.x * G) {
+        uint32_t key[G];
+        float4 xv[G][DP / 4];
+        int32_t av[G], pv[G];
+        float uv[G];
 #pragma unroll
-        for (int j = 0; j < DP / 4; ++j) dx[j] = __ldg(src + j);
-        p.a2[dst] = p.a[r];
-        p.u2[dst] = p.u[r];
-        p.perm2[dst] = p.perm[r];
+        for (int g = 0; g < G; ++g) {
+            const int64_t r = rb + 32 * g + lane;
+            const bool v = r < r1;
+            key[g] = v ? __ldg(p.keys + r) : 0xffffffffu;
+            const float4 *src = reinterpret_cast<const float4 *>(p.X + (v ? r : r0) * DP);
+#pragma unroll
+            for (int j = 0; j < DP / 4; ++j) xv[g][j] = __ldg(src + j);
+            av[g] = __ldg(p.a + (v ? r : r0));
+            uv[g] = __ldg(p.u + (v ? r : r0));
+            pv[g] = __ldg(p.perm + (v ? r : r0));
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const bool v = key[g] != 0xffffffffu;
+            const unsigned grp = __match_any_sync(kFull, key[g]);
+            const int leader = __ffs(grp) - 1;
+            uint32_t base = 0;
+            if (v && lane == leader) base = atomicAdd(&cur[key[g]], (uint32_t)__popc(grp));
+            base = __shfl_sync(kFull, base, leader);
+            if (!v) continue;
+            const int64_t dst = base + __popc(grp & ((1u << lane) - 1u));
+            float4 *dx = reinterpret_cast<float4 *>(p.X2 + dst * DP);
+#pragma unroll
+            for (int j = 0; j < DP / 4; ++j) dx[j] = xv[g][j];
+            p.a2[dst] = av[g];
+            p.u2[dst] = uv[g];
+            p.perm2[dst] = pv[g];
+        }
     }
 }
 
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches)
 {
     const size_t sh = (size_t)p.NB * sizeof(uint32_t);   // NB <= 4096 -> <= 16 KB
-    k_sort_keys<<<p.ntiles, 512, sh, st>>>(p);
+    const size_t shk = sh + (p.Q > 1 && p.k <= kSortSmemK ? (size_t)p.k * p.k * sizeof(float) : 0);
+    if (shk > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_sort_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shk);
+        if (e != cudaSuccess) return e;
+    }
+    k_sort_keys<<<p.ntiles, 512, shk, st>>>(p);
     k_scan_tiles<<<p.NB, 1024, 0, st>>>(p);
     k_scan_buckets<<<1, 1024, 0, st>>>(p);
     switch (p.DP) {
