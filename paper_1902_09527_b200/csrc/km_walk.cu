@@ -106,8 +106,11 @@ __device__ __forceinline__ void move_delta(double *acc, int d, int a, int b, con
 
 // One lane = R rows (rows r0 + lane + 32 i); the warp walks its cluster A's candidate rows once
 // for all 32 R rows, so each broadcast load serves R rows per lane.
+// resident CTAs per SM the register budget allows without spills (80 / 128 / 255 registers)
+template <int DP> constexpr int walk_minb() { return DP <= 8 ? 3 : (DP <= 32 ? 2 : 1); }
+
 template <int DP, bool CSMEM, int R, int NH, bool HSMEM>
-__global__ void __launch_bounds__(kWalkThreads, 3)
+__global__ void __launch_bounds__(kWalkThreads, walk_minb<DP>())
 k_walk(AssignParams p)
 {
     extern __shared__ __align__(16) float smem[];
@@ -295,14 +298,40 @@ k_walk(AssignParams p)
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 if (!active[i]) continue;
-                // rigorous decision (same procedure as the tensor-core epilogue)
+                // rigorous decision (same procedure as the tensor-core epilogue).  Fast paths in
+                // the squared domain: a key value v with v > thr = (u_t + epsr)^2 + E has a lower
+                // distance bound above u_t, the upper bound of the own cluster's distance.
                 const float E = __fmul_ru(kappa, __fadd_ru(xx[i], cmax));
                 const float epsr = __fadd_ru(eps, __fmul_ru(1.2e-7f, __fadd_ru(sqrt_up(xx[i]), sqrt_up(cmax))));
                 const float ue = __fadd_ru(ut[i], epsr);
                 const float thr = __fadd_ru(__fmul_ru(ue, ue), E);
-                bool fallback = false;
-                if (!misfit[i] && (m1[i] == 0x7fffffff || __int_as_float(m1[i] & kmask) > thr)) {
-                    unew[i] = ut[i];                             // stays (common case)
+                const float v1 = m1[i] == 0x7fffffff ? INFINITY : __int_as_float(m1[i] & kmask);
+                const float v2 = m2[i] == 0x7fffffff ? INFINITY : __int_as_float(m2[i] & kmask);
+                bool fallback = false, stay;
+                if (!misfit[i]) {
+                    stay = v1 > thr;
+                } else {
+                    // misfit: stays if A is farther than u_t and every candidate but the own
+                    // cluster's column is: either all keys exceed thr, or only the best does not
+                    // and the best is the own cluster (then any other key is >= m2 > thr)
+                    const bool a_far = __fmul_rd(sqrt_dn(xx[i]), p.g_dn) > __fadd_ru(ut[i], eps);
+                    stay = a_far && (v1 > thr ||
+                                     (v2 > thr && __float_as_int(__ldg(&mA[m1[i] & ~kmask].y)) == aold[i]));
+                }
+                if (stay) {
+                    unew[i] = ut[i];
+                } else if (!misfit[i]) {
+                    // moves to the best candidate if its interval is clear of the own cluster's
+                    // and of every other candidate's (>= m2)
+                    const float U1 = __fadd_ru(sqrt_up(__fadd_ru(__fmul_ru(fmaxf(v1, 0.f), qtrunc), E)), epsr);
+                    const float L2 = v2 == INFINITY ? INFINITY
+                                                    : fmaxf(0.f, __fsub_rd(sqrt_dn(fmaxf(__fsub_rd(v2, E), 0.f)), epsr));
+                    if (U1 < fminf(lo[i], L2)) {
+                        anew[i] = __float_as_int(__ldg(&mA[m1[i] & ~kmask].y));
+                        unew[i] = U1;
+                    } else {
+                        fallback = true;
+                    }
                 } else {
                     auto U_of = [&](int key) {
                         const float v = fmaxf(__int_as_float(key & kmask), 0.f);
@@ -317,7 +346,7 @@ k_walk(AssignParams p)
                     const int cc2 = m2[i] != 0x7fffffff ? __float_as_int(__ldg(&mA[m2[i] & ~kmask].y)) : -1;
                     float Uo = ut[i], Lo = lo[i], Ui = INFINITY, Li = INFINITY, Lother = INFINITY;
                     int ci = -1;
-                    if (cc1 == aold[i]) {      // (misfit) own cluster is the best candidate: merge
+                    if (cc1 == aold[i]) {      // own cluster is the best candidate: merge
                         Uo = fminf(Uo, U_of(m1[i])); Lo = fmaxf(Lo, L_of(m1[i]));
                         ci = cc2;
                         if (ci >= 0) { Ui = U_of(m2[i]); Li = L_of(m2[i]); Lother = -1.f; }   // third unknown
@@ -326,11 +355,10 @@ k_walk(AssignParams p)
                         if (ci >= 0) { Ui = U_of(m1[i]); Li = L_of(m1[i]); }
                         Lother = L_of(m2[i]);
                     }
-                    float UA = INFINITY, LA = INFINITY;
-                    if (misfit[i]) { UA = upper_d(xx[i], p.g_up, eps); LA = lower_d(xx[i], p.g_dn, eps); }
+                    const float UA = upper_d(xx[i], p.g_up, eps), LA = lower_d(xx[i], p.g_dn, eps);
                     if (Uo < fminf(Li, LA)) {
                         unew[i] = Uo;
-                    } else if (misfit[i] && UA < fminf(Lo, Li)) {
+                    } else if (UA < fminf(Lo, Li)) {
                         anew[i] = A; unew[i] = UA;
                     } else if (ci >= 0 && Ui < fminf(fminf(Lo, LA), Lother)) {
                         anew[i] = ci; unew[i] = Ui;
