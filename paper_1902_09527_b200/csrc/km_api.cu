@@ -493,9 +493,16 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     KM_CUDA(cudaMallocHost(&c->hstat, sizeof(HostStat)));
     // points -> private padded copy
     float *X0 = c->X[0];
-    KM_CUDA(cudaMemcpy2DAsync(X0, DP * sizeof(float), points, d * sizeof(float), d * sizeof(float),
-                              (size_t)n, o->points_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                              c->st));
+    const cudaMemcpyKind kind = o->points_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    if (DP == d) {
+        // one linear copy (a pitched copy of 32-byte rows runs far below the link bandwidth)
+        KM_CUDA(cudaMemcpyAsync(X0, points, (size_t)n * d * sizeof(float), kind, c->st));
+    } else {
+        // linear copy into the second buffer, then pad d -> DP on the device
+        KM_CUDA(cudaMemcpyAsync(c->X[1], points, (size_t)n * d * sizeof(float), kind, c->st));
+        KM_CUDA(km::launch_pad_rows(c->X[1], X0, n, d, DP, c->st));
+        c->launches += 1;
+    }
     KM_CUDA(km::launch_iota(c->perm[0], n, c->st));
     c->launches += 1;
     KM_CUDA(cudaMemcpyAsync(c->C, C0, (size_t)k * d * sizeof(double), cudaMemcpyHostToDevice, c->st));

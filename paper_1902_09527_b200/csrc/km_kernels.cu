@@ -673,6 +673,23 @@ cudaError_t launch_unpermute(const int32_t *a, const int32_t *perm, int64_t n, i
     return cudaGetLastError();
 }
 
+// X (n x d, contiguous) -> Xp (n x DP, zero padded)
+__global__ void k_pad_rows(const float *X, float *Xp, int64_t n, int d, int DP)
+{
+    const int64_t tot = n * DP;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / DP;
+        const int j = (int)(i - r * DP);
+        Xp[i] = j < d ? X[r * d + j] : 0.f;
+    }
+}
+
+cudaError_t launch_pad_rows(const float *X, float *Xp, int64_t n, int d, int DP, cudaStream_t st)
+{
+    k_pad_rows<<<148 * 8, 256, 0, st>>>(X, Xp, n, d, DP);
+    return cudaGetLastError();
+}
+
 __global__ void k_iota(int32_t *perm, int64_t n)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;

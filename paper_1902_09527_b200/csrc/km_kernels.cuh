@@ -123,6 +123,7 @@ cudaError_t launch_sse(const float *X, const int32_t *a, const double *C, int64_
 cudaError_t launch_unpermute(const int32_t *a, const int32_t *perm, int64_t n, int32_t *out,
                              cudaStream_t st);
 cudaError_t launch_iota(int32_t *perm, int64_t n, cudaStream_t st);
+cudaError_t launch_pad_rows(const float *X, float *Xp, int64_t n, int d, int DP, cudaStream_t st);
 cudaError_t launch_check_finite(const float *X, int64_t count, int *flag, cudaStream_t st);
 
 }  // namespace km
