@@ -143,7 +143,7 @@ k_walk(AssignParams p)
     double *acc = p.acc + (int64_t)(blockIdx.x % p.nslab) * k * (DP + 1);
     const float eps = *p.eps;
     const int lane = threadIdx.x & 31;
-    const int64_t n = p.n;
+    const int n = (int)p.n;                        // < 2^31 (kmeans_create enforces it)
     const int kp = p.wpad;                          // candidate rows per cluster block
     const int kcols = k - 1;
     const int ib = p.wbits;                         // key index bits
@@ -157,16 +157,17 @@ k_walk(AssignParams p)
     unsigned long long steps = 0;
 
     constexpr int kBatches = kWalkChunk / kRows;
-    auto claim = [&]() -> int64_t {
+    auto claim = [&]() -> int {
         int c = 0;
         if (lane == 0) c = atomicAdd(p.work, 1);
-        return (int64_t)__shfl_sync(kFull, c, 0) * kWalkChunk;
+        c = __shfl_sync(kFull, c, 0);
+        return c < (n + kWalkChunk - 1) / kWalkChunk ? c * kWalkChunk : n;   // n: no more work
     };
-    int64_t chunk_row = claim(), ahead_row = claim();
+    int chunk_row = claim(), ahead_row = claim();
     int bt = 0;
     // stage rows [r0, r0 + 32 R) of X, a, u into this warp's buffer (16-B cp.async per lane)
-    auto stage = [&](int64_t r0) {
-        const float4 *xs = reinterpret_cast<const float4 *>(p.X + r0 * DP);
+    auto stage = [&](int r0) {
+        const float4 *xs = reinterpret_cast<const float4 *>(p.X + (size_t)r0 * DP);
         float4 *xd = reinterpret_cast<float4 *>(stg);
 #pragma unroll
         for (int c = lane; c < kRowsB * DP / 4; c += 32) cp_async16(xd + c, xs + c);
@@ -178,7 +179,7 @@ k_walk(AssignParams p)
     if (chunk_row < n) stage(chunk_row);
 
     while (chunk_row < n) {
-        const int64_t row0 = chunk_row + bt * kRows;
+        const int row0 = chunk_row + bt * kRows;
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
         float x[R][DP];
@@ -196,7 +197,7 @@ k_walk(AssignParams p)
             }
             aold[i] = __float_as_int(stg[kRowsB * DP + r]);
             const float uold = stg[kRowsB * DP + kRowsB + r];
-            const int64_t row = row0 + r;
+            const int row = row0 + r;
             valid[i] = row < n;
             if (!valid[i]) aold[i] = 0;
             uu[i] = valid[i] ? __fadd_ru(uold, sF[aold[i]]) : 0.f;          // u += f(a)
@@ -371,7 +372,7 @@ k_walk(AssignParams p)
                     const uint64_t *nl = p.NL + (int64_t)aold[i] * p.ks;
                     float xr[DP];
                     {
-                        const float4 *src = reinterpret_cast<const float4 *>(p.X + (row0 + 32 * i + lane) * DP);
+                        const float4 *src = reinterpret_cast<const float4 *>(p.X + (size_t)(row0 + 32 * i + lane) * DP);
 #pragma unroll
                         for (int j = 0; j < DP / 4; ++j) {
                             const float4 t = __ldg(src + j);
@@ -391,7 +392,7 @@ k_walk(AssignParams p)
                     }
                     const float ub = upper_d(bq, p.g_up, eps);
                     if (q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub) {
-                        anew[i] = refine64(p.X + (row0 + 32 * i + lane) * DP, p.d, p.C64, k, aold[i], nl, ut[i], &unew[i]);
+                        anew[i] = refine64(p.X + (size_t)(row0 + 32 * i + lane) * DP, p.d, p.C64, k, aold[i], nl, ut[i], &unew[i]);
                         ++c_refined;
                     } else {
                         anew[i] = bc;
@@ -410,7 +411,7 @@ k_walk(AssignParams p)
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-            const int64_t rb = row0 + 32 * i;
+            const int rb = row0 + 32 * i;
             if constexpr (!HSMEM) {   // deferred counts: per 32-row group: defer[rb + i], dcount[rb / 32]
                 const unsigned dm = __ballot_sync(kFull, defer[i]);
                 if (defer[i])
@@ -424,7 +425,7 @@ k_walk(AssignParams p)
                 if (anew[i] != aold[i]) {
                     ++c_changed;
                     float xr[DP];
-                    const float4 *src = reinterpret_cast<const float4 *>(p.X + (rb + lane) * DP);
+                    const float4 *src = reinterpret_cast<const float4 *>(p.X + (size_t)(rb + lane) * DP);
 #pragma unroll
                     for (int j = 0; j < DP / 4; ++j) {
                         const float4 t = __ldg(src + j);
