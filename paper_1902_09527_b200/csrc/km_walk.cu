@@ -35,6 +35,14 @@ constexpr int kWalkChunk = 256;        // rows a warp claims per work-counter fe
 
 __host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // float4 per candidate pair
 
+// 32-byte read-only load (LDG.E.ENL2.256): two float4 in one instruction
+__device__ __forceinline__ void ldg256(const float4 *src, float4 &a, float4 &b)
+{
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(src));
+}
+
 // FFMA2 with a scalar operand broadcast to both lanes: r = (a*b.x + c.x, a*b.y + c.y)
 __device__ __forceinline__ float2 fma2s(float a, float2 b, float2 c)
 {
@@ -278,8 +286,14 @@ k_walk(AssignParams p)
             for (int i = 0; i < R; ++i) { m1[i] = 0x7fffffff; m2[i] = 0x7fffffff; }
             for (int j = 0; j < pm; j += 2) {
                 float4 v[DP / 2];
+                if constexpr (DP >= 32) {   // halves the load instructions where they dominate
 #pragma unroll
-                for (int e = 0; e < DP / 2; ++e) v[e] = __ldg(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e);
+                    for (int e = 0; e < DP / 2; e += 2)
+                        ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e, v[e], v[e + 1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < DP / 2; ++e) v[e] = __ldg(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e);
+                }
                 const float2 cc = __ldg(ccA + (j >> 1));
 #pragma unroll
                 for (int i = 0; i < R; ++i) {
