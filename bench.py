@@ -279,7 +279,7 @@ def run_ours(args, rank, world, local_rank):
         Xh = torch.empty((hi - lo, d), dtype=torch.float32, pin_memory=True)
         Xh.numpy()[:] = X
         total_iters = args.warmup + args.steps
-        a_out = np.empty(hi - lo, np.int32)
+        a_out = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)   # caller-owned, pinned
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -288,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
                      device=local_rank)
         for _ in range(total_iters):
             km2.iterate()
-        a_out[:] = km2.assignments()
+        km2.assignments(out=a_out)
         C_out = km2.centroids()
         t_e2e = time.perf_counter() - t0
         km2.close()

@@ -464,6 +464,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         KM_CUDA(cudaMemsetAsync(c->u[i], 0, (size_t)c->n_alloc * sizeof(float), c->st));
     }
     c->Q = std::max(1, std::min(32, 4096 / k));
+    if (const char *e = getenv("KM_Q")) c->Q = std::max(1, std::min(c->Q, atoi(e)));
     const int NBmax = k * c->Q;
     c->ntiles = (int)((n + c->tile_rows - 1) / c->tile_rows);
     KM_TRY(dalloc(&c->keys, (size_t)n));

@@ -98,9 +98,14 @@ class KMeans:
 
     # -- results -------------------------------------------------------------------------------
     def assignments(self, out=None):
-        """int32[n_local] in the caller's row order.  ``out`` may be a CUDA int32 tensor."""
+        """int32[n_local] in the caller's row order.  ``out`` may be an int32 torch tensor on the
+        context's device or in (preferably pinned) host memory, or an int32 numpy array."""
         if out is not None:
-            C.check(C.lib().kmeans_get_assignments(self._h, ct.c_void_p(out.data_ptr()), 1))
+            if hasattr(out, "data_ptr"):
+                on_dev = 1 if getattr(out, "is_cuda", False) else 0
+                C.check(C.lib().kmeans_get_assignments(self._h, ct.c_void_p(out.data_ptr()), on_dev))
+            else:
+                C.check(C.lib().kmeans_get_assignments(self._h, ct.c_void_p(out.ctypes.data), 0))
             return out
         a = np.empty(self.n, np.int32)
         C.check(C.lib().kmeans_get_assignments(self._h, ct.c_void_p(a.ctypes.data), 0))
