@@ -348,7 +348,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
     KM_TRY(prep(c));
     KM_CUDA(cudaEventRecord(ev[2], c->st));
-    c->delta_pass = !first && c->use_walk;
+    c->delta_pass = !first && (c->use_walk || c->use_tc);
     if (first) {
         KM_TRY(launch_assign(c, km::MODE_DENSE, 0));
         KM_CUDA(cudaEventRecord(ev[3], c->st));

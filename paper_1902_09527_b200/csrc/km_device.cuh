@@ -243,4 +243,20 @@ __device__ __forceinline__ void reduce_batch(RunAcc<DP> &ra, const float (&x)[DP
 }
 
 
+// fp64 delta reduction of a row that moved from a to b: S[b] += x, S[a] -= x (counts +-1)
+template <int DP>
+__device__ __forceinline__ void move_delta(double *acc, int d, int a, int b, const float (&x)[DP])
+{
+    double *ra = acc + (int64_t)a * (DP + 1), *rb = acc + (int64_t)b * (DP + 1);
+#pragma unroll
+    for (int j = 0; j < DP; ++j)
+        if (j < d) {
+            const double v = (double)x[j];
+            atomicAdd(rb + j, v);
+            atomicAdd(ra + j, -v);
+        }
+    atomicAdd(rb + DP, 1.0);
+    atomicAdd(ra + DP, -1.0);
+}
+
 }  // namespace km

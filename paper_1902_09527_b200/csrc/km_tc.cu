@@ -89,9 +89,10 @@ __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count)
 
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase)
 {
+    // suspend-time hint: a waiting warp sleeps until the phase completes instead of spinning
     asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-                 "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}" :: "r"(mbar), "r"(phase) : "memory");
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+                 "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}" :: "r"(mbar), "r"(phase), "r"(1000000) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_tx(uint32_t mbar, uint32_t bytes)
@@ -489,8 +490,6 @@ k_mti_tc(AssignParams p, TcCfg L)
         CRow<CSMEM> Cn;
         if constexpr (CSMEM) Cn.base = tc::smem_u32(sC); else Cn.base = p.Cneg;
         double *acc = p.acc + (int64_t)(blockIdx.x % p.nslab) * k * (DP + 1);
-        RunAcc<DP> ra;
-        ra.clear();
         unsigned long long c_changed = 0, c_dists = 0, c_refined = 0, c_cols = 0, c_fb = 0;
         uint32_t qid[16];                             // column ids 0..15 kept in registers
 #pragma unroll
@@ -642,11 +641,10 @@ k_mti_tc(AssignParams p, TcCfg L)
                 p.u[row] = unew;
                 c_changed += (anew != st.a);
             }
-            reduce_batch<DP>(ra, x, anew, valid, acc, p.d, lane);
+            if (valid && anew != st.a) move_delta<DP>(acc, p.d, st.a, anew, x);   // S3 as a delta (B5)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_sfree[s]));     // stage reusable
         }
-        ra.flush(acc, p.d, lane);
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) {
             c_changed += __shfl_xor_sync(kFull, c_changed, o);

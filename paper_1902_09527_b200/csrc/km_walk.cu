@@ -96,22 +96,6 @@ __device__ __forceinline__ int count_below_f(const float *__restrict__ h, int m,
     return lo;
 }
 
-// fp64 delta reduction of a row that moved from a to b: S[b] += x, S[a] -= x (counts +-1)
-template <int DP>
-__device__ __forceinline__ void move_delta(double *acc, int d, int a, int b, const float (&x)[DP])
-{
-    double *ra = acc + (int64_t)a * (DP + 1), *rb = acc + (int64_t)b * (DP + 1);
-#pragma unroll
-    for (int j = 0; j < DP; ++j)
-        if (j < d) {
-            const double v = (double)x[j];
-            atomicAdd(rb + j, v);
-            atomicAdd(ra + j, -v);
-        }
-    atomicAdd(rb + DP, 1.0);
-    atomicAdd(ra + DP, -1.0);
-}
-
 // One lane = R rows (rows r0 + lane + 32 i); the warp walks its cluster A's candidate rows once
 // for all 32 R rows, so each broadcast load serves R rows per lane.
 // resident CTAs per SM the register budget allows without spills (80 / 128 / 255 registers)
