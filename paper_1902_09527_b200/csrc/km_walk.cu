@@ -169,6 +169,22 @@ k_walk(AssignParams p)
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if (chunk_row < n) stage(chunk_row);
+    // mover queue (registers, lane l holds entry l < mq)
+    int mrow = 0, mfrom = 0, mto = 0, mq = 0;
+    auto flush_moves = [&]() {
+        if (lane < mq) {
+            float xr[DP];
+            const float4 *src = reinterpret_cast<const float4 *>(p.X + (size_t)mrow * DP);
+#pragma unroll
+            for (int j = 0; j < DP / 4; ++j) {
+                const float4 t = __ldg(src + j);
+                xr[4 * j] = t.x; xr[4 * j + 1] = t.y; xr[4 * j + 2] = t.z; xr[4 * j + 3] = t.w;
+            }
+            move_delta<DP>(acc, p.d, mfrom, mto, xr);
+        }
+        __syncwarp();
+        mq = 0;
+    };
 
     while (chunk_row < n) {
         const int row0 = chunk_row + bt * kRows;
@@ -420,20 +436,34 @@ k_walk(AssignParams p)
             if (valid[i]) {
                 p.a[rb + lane] = anew[i];
                 p.u[rb + lane] = unew[i];
-                if (anew[i] != aold[i]) {
-                    ++c_changed;
-                    float xr[DP];
-                    const float4 *src = reinterpret_cast<const float4 *>(p.X + (size_t)(rb + lane) * DP);
-#pragma unroll
-                    for (int j = 0; j < DP / 4; ++j) {
-                        const float4 t = __ldg(src + j);
-                        xr[4 * j] = t.x; xr[4 * j + 1] = t.y; xr[4 * j + 2] = t.z; xr[4 * j + 3] = t.w;
+            }
+            // S3 as a delta (B5): movers are queued in registers (one per lane) and their fp64
+            // deltas applied 32 at a time, so the REDs run with full warps
+            {
+                const bool mv = valid[i] && anew[i] != aold[i];
+                const unsigned mm = __ballot_sync(kFull, mv);
+                if (mm) {
+                    c_changed += mv;
+                    const int m = __popc(mm);
+                    const int packed = (rb + lane);
+                    int taken = 0;
+                    while (taken < m) {
+                        const int t = min(32 - mq, m - taken);
+                        const bool dst = lane >= mq && lane < mq + t;
+                        const int src = dst ? (int)__fns(mm, 0, taken + (lane - mq) + 1) : lane;
+                        const int r_ = __shfl_sync(kFull, packed, src);
+                        const int ao = __shfl_sync(kFull, aold[i], src);
+                        const int an = __shfl_sync(kFull, anew[i], src);
+                        if (dst) { mrow = r_; mfrom = ao; mto = an; }
+                        mq += t;
+                        taken += t;
+                        if (mq == 32) flush_moves();
                     }
-                    move_delta<DP>(acc, p.d, aold[i], anew[i], xr);     // S3 as a delta
                 }
             }
         }
     }
+    flush_moves();
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         c_changed += __shfl_xor_sync(kFull, c_changed, o);
