@@ -99,7 +99,7 @@ __device__ __forceinline__ int count_below_f(const float *__restrict__ h, int m,
 // One lane = R rows (rows r0 + lane + 32 i); the warp walks its cluster A's candidate rows once
 // for all 32 R rows, so each broadcast load serves R rows per lane.
 // resident CTAs per SM the register budget allows without spills (80 / 128 / 255 registers)
-template <int DP> constexpr int walk_minb() { return DP <= 8 ? 3 : (DP <= 32 ? 2 : 1); }
+template <int DP> constexpr int walk_minb() { return DP <= 8 ? 3 : (DP <= 16 ? 2 : 1); }
 
 template <int DP, bool CSMEM, int R, int NH, bool HSMEM>
 __global__ void __launch_bounds__(kWalkThreads, walk_minb<DP>())
@@ -528,14 +528,14 @@ cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, 
 
 size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem)
 {
-    const int R = DP <= 16 ? 2 : 1;
+    const int R = DP <= 32 ? 2 : 1;
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
            (size_t)(kWalkThreads / 32) * 32 * R * (DP + 2) * sizeof(float);
 }
 
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
-template <int DP> constexpr int walk_r() { return DP <= 16 ? 2 : 1; }
+template <int DP> constexpr int walk_r() { return DP <= 32 ? 2 : 1; }
 
 typedef void (*walk_kernel_t)(AssignParams);
 
