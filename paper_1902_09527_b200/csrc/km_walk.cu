@@ -30,7 +30,8 @@
 
 namespace km {
 
-constexpr int kWalkThreads = 256;
+// One CTA per SM: the shared H rows and C are held once per SM rather than once per CTA, which
+// leaves most of the 256 KB L1/shared array as L1 for the candidate tables (walk_threads below).
 constexpr int kWalkChunk = 256;        // rows a warp claims per work-counter fetch
 
 __host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // float4 per candidate pair
@@ -54,13 +55,24 @@ __device__ __forceinline__ float2 fma2s(float a, float2 b, float2 c)
     return r;
 }
 
+// FADD2 with a scalar operand broadcast to both lanes: r = (a + b.x, a + b.y)
+__device__ __forceinline__ float2 add2s(float a, float2 b)
+{
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rr;\n\t"
+        "mov.b64 ra, {%2, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+        "add.rn.f32x2 rr, ra, rb;\n\tmov.b64 {%0, %1}, rr;\n\t}"
+        : "=f"(r.x), "=f"(r.y) : "f"(a), "f"(b.x), "f"(b.y));
+    return r;
+}
+
 // squared distances to the candidate pair (j, j+1) in the centred expansion form:
 // (q_j, q_j+1) = (xx + cc_j, xx + cc_j+1) + sum_e x'_e (m_j[e], m_j+1[e]),  m = -2 c'
 // v: the pair's DP/2 float4 (coordinates interleaved by candidate); one FFMA2 per coordinate
 template <int DP>
 __device__ __forceinline__ float2 q_pair(const float (&xc)[DP], float xx, float2 cc, const float4 (&v)[DP / 2])
 {
-    float2 s = make_float2(xx + cc.x, xx + cc.y);
+    float2 s = add2s(xx, cc);
 #pragma unroll
     for (int e = 0; e < DP / 2; ++e) {
         s = fma2s(xc[2 * e], make_float2(v[e].x, v[e].y), s);
@@ -78,6 +90,29 @@ __device__ __forceinline__ int count_below_u(P h, float T)
     for (int half = NH >> 1; half >= 1; half >>= 1)
         base = h[base + half - 1] < T ? base + half : base;
     return base + (h[base] < T ? 1 : 0);
+}
+
+// shared-memory form: the running lower bound is kept as a byte address, so each step is one
+// LDS with an immediate offset, one compare and one predicated add
+template <int HALF>
+__device__ __forceinline__ void cbs_step(uint32_t &a, float T)
+{
+    if constexpr (HALF >= 1) {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"((HALF - 1) * 4));
+        if (v < T) a += HALF * 4;
+        cbs_step<HALF / 2>(a, T);
+    }
+}
+template <int NH>
+__device__ __forceinline__ int count_below_s(const float *h, float T)
+{
+    const uint32_t a0 = (uint32_t)__cvta_generic_to_shared(h);
+    uint32_t a = a0;
+    cbs_step<NH / 2>(a, T);
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return (int)((a - a0) >> 2) + (v < T ? 1 : 0);
 }
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src)
@@ -100,9 +135,12 @@ __device__ __forceinline__ int count_below_f(const float *__restrict__ h, int m,
 // for all 32 R rows, so each broadcast load serves R rows per lane.
 // resident CTAs per SM the register budget allows without spills (80 / 128 / 255 registers)
 template <int DP> constexpr int walk_minb() { return DP <= 8 ? 3 : (DP <= 16 ? 2 : 1); }
+// threads per CTA: the warps of walk_minb 256-thread CTAs fused into one (same register cap)
+template <int DP> constexpr int walk_threads() { return 256 * walk_minb<DP>(); }
+static int walk_threads_rt(int DP) { return DP <= 8 ? 768 : (DP <= 16 ? 512 : 256); }
 
 template <int DP, bool CSMEM, int R, int NH, bool HSMEM>
-__global__ void __launch_bounds__(kWalkThreads, walk_minb<DP>())
+__global__ void __launch_bounds__(walk_threads<DP>(), 1)
 k_walk(AssignParams p)
 {
     extern __shared__ __align__(16) float smem[];
@@ -272,7 +310,7 @@ k_walk(AssignParams p)
                         lo[i] = lower_d(qo, p.g_dn, eps);
                         T[i] = __fmul_ru(__fadd_ru(ut[i], upper_d(xx[i], p.g_up, eps)), 0.5f);
                     }
-                    if constexpr (HSMEM) pl[i] = count_below_u<NH>(sH + A * NH, T[i]);
+                    if constexpr (HSMEM) pl[i] = count_below_s<NH>(sH + A * NH, T[i]);
                     else pl[i] = count_below_u<NH>(p.WH + (int64_t)A * NH, T[i]);
                 }
                 pm = max(pm, pl[i]);
@@ -417,7 +455,7 @@ k_walk(AssignParams p)
                 if (!misfit[i]) {
                     c_dists += (unsigned long long)(1 + pl[i]);
                 } else if constexpr (HSMEM) {      // own list's H row is in shared memory
-                    c_dists += (unsigned long long)(1 + count_below_u<NH>(sH + aold[i] * NH, ut[i]));
+                    c_dists += (unsigned long long)(1 + count_below_s<NH>(sH + aold[i] * NH, ut[i]));
                 } else {
                     defer[i] = true;                 // counted by k_mti_count
                 }
@@ -531,7 +569,7 @@ size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem)
     const int R = DP <= 32 ? 2 : 1;
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
-           (size_t)(kWalkThreads / 32) * 32 * R * (DP + 2) * sizeof(float);
+           (size_t)(walk_threads_rt(DP) / 32) * 32 * R * (DP + 2) * sizeof(float);
 }
 
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
@@ -591,7 +629,7 @@ cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, cud
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, kWalkThreads, sm, st>>>(p);
+    kern<<<grid, walk_threads_rt(DP), sm, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -602,7 +640,7 @@ int walk_grid(int DP, bool csmem, int k, int whs, bool hs, int num_sms)
     const size_t sm = walk_smem(DP, csmem, k, whs, hs);
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWalkThreads, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, walk_threads_rt(DP), sm);
     return (per_sm < 1 ? 1 : per_sm) * num_sms;
 }
 
