@@ -33,6 +33,7 @@ namespace km {
 // One CTA per SM: the shared H rows and C are held once per SM rather than once per CTA, which
 // leaves most of the 256 KB L1/shared array as L1 for the candidate tables (walk_threads below).
 constexpr int kWalkChunk = 256;        // rows a warp claims per work-counter fetch
+constexpr int kQueue = 64;             // mover-queue entries per warp (< 32 left + 32 new)
 
 __host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // float4 per candidate pair
 
@@ -152,7 +153,8 @@ k_walk(AssignParams p)
     float *sH = sS + k4;                            // k x NH H rows (HSMEM)
     // per-warp staging of the next batch (cp.async): x rows, then a, then u
     constexpr int kRowsB = 32 * R;
-    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2));
+    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2) + 3 * kQueue);
+    int *sQ = reinterpret_cast<int *>(stg + kRowsB * DP + 2 * kRowsB);   // mover queue: row, from, to
     if (CSMEM) {
         const float4 *src = reinterpret_cast<const float4 *>(p.Cneg);
         float4 *dst = reinterpret_cast<float4 *>(sC);
@@ -207,10 +209,12 @@ k_walk(AssignParams p)
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if (chunk_row < n) stage(chunk_row);
-    // mover queue (registers, lane l holds entry l < mq)
-    int mrow = 0, mfrom = 0, mto = 0, mq = 0;
+    // mover queue (shared memory, kQueue entries per warp; mq warp-uniform)
+    int mq = 0;
     auto flush_moves = [&]() {
-        if (lane < mq) {
+        __syncwarp();
+        if (lane < min(mq, 32)) {
+            const int mrow = sQ[lane], mfrom = sQ[kQueue + lane], mto = sQ[2 * kQueue + lane];
             float xr[DP];
             const float4 *src = reinterpret_cast<const float4 *>(p.X + (size_t)mrow * DP);
 #pragma unroll
@@ -221,7 +225,17 @@ k_walk(AssignParams p)
             move_delta<DP>(acc, p.d, mfrom, mto, xr);
         }
         __syncwarp();
-        mq = 0;
+        if (mq > 32) {   // keep the overflow (< 32 entries) at the front
+            int e0 = 0, e1 = 0, e2 = 0;
+            const bool mv = lane < mq - 32;
+            if (mv) { e0 = sQ[32 + lane]; e1 = sQ[kQueue + 32 + lane]; e2 = sQ[2 * kQueue + 32 + lane]; }
+            __syncwarp();
+            if (mv) { sQ[lane] = e0; sQ[kQueue + lane] = e1; sQ[2 * kQueue + lane] = e2; }
+            __syncwarp();
+            mq -= 32;
+        } else {
+            mq = 0;
+        }
     };
 
     while (chunk_row < n) {
@@ -475,28 +489,19 @@ k_walk(AssignParams p)
                 p.a[rb + lane] = anew[i];
                 p.u[rb + lane] = unew[i];
             }
-            // S3 as a delta (B5): movers are queued in registers (one per lane) and their fp64
+            // S3 as a delta (B5): movers are queued in shared memory and their fp64
             // deltas applied 32 at a time, so the REDs run with full warps
             {
                 const bool mv = valid[i] && anew[i] != aold[i];
                 const unsigned mm = __ballot_sync(kFull, mv);
                 if (mm) {
                     c_changed += mv;
-                    const int m = __popc(mm);
-                    const int packed = (rb + lane);
-                    int taken = 0;
-                    while (taken < m) {
-                        const int t = min(32 - mq, m - taken);
-                        const bool dst = lane >= mq && lane < mq + t;
-                        const int src = dst ? (int)__fns(mm, 0, taken + (lane - mq) + 1) : lane;
-                        const int r_ = __shfl_sync(kFull, packed, src);
-                        const int ao = __shfl_sync(kFull, aold[i], src);
-                        const int an = __shfl_sync(kFull, anew[i], src);
-                        if (dst) { mrow = r_; mfrom = ao; mto = an; }
-                        mq += t;
-                        taken += t;
-                        if (mq == 32) flush_moves();
+                    if (mv) {
+                        const int slot = mq + __popc(mm & ((1u << lane) - 1u));
+                        sQ[slot] = rb + lane; sQ[kQueue + slot] = aold[i]; sQ[2 * kQueue + slot] = anew[i];
                     }
+                    mq += __popc(mm);
+                    if (mq >= 32) flush_moves();
                 }
             }
         }
@@ -569,7 +574,7 @@ size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem)
     const int R = DP <= 32 ? 2 : 1;
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
-           (size_t)(walk_threads_rt(DP) / 32) * 32 * R * (DP + 2) * sizeof(float);
+           (size_t)(walk_threads_rt(DP) / 32) * (32 * R * (DP + 2) + 3 * kQueue) * sizeof(float);
 }
 
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
