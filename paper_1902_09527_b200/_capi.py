@@ -10,7 +10,8 @@ import ctypes as ct
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_PKG, "libkmeans_b200.so")
+# KM_LIB: an alternative build of the same library (A/B kernel variants, tools/build_variant.py)
+SO_PATH = os.environ.get("KM_LIB") or os.path.join(_PKG, "libkmeans_b200.so")
 
 KM_OK, KM_EARG, KM_ENONFINITE, KM_ECUDA, KM_ENCCL, KM_ENOMEM, KM_ESTATE = range(7)
 KM_PRUNE_MTI, KM_PRUNE_NONE = 0, 1

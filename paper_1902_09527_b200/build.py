@@ -26,17 +26,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile the library (``out``/``defines``: an A/B variant, see tools/build_variant.py)."""
+    so = out or SO
+    if out is None and not force and not needs_build():
         return SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-o", SO + ".tmp", *SRCS, "-ldl"]
+           "-I", os.path.join(ROOT, "include"), *[f"-D{x}" for x in defines], "-o", so + ".tmp", *SRCS, "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":

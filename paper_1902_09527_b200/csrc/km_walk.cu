@@ -134,11 +134,24 @@ __device__ __forceinline__ int count_below_f(const float *__restrict__ h, int m,
 
 // One lane = R rows (rows r0 + lane + 32 i); the warp walks its cluster A's candidate rows once
 // for all 32 R rows, so each broadcast load serves R rows per lane.
-// resident CTAs per SM the register budget allows without spills (80 / 128 / 255 registers)
-template <int DP> constexpr int walk_minb() { return DP <= 8 ? 3 : (DP <= 16 ? 2 : 1); }
-// threads per CTA: the warps of walk_minb 256-thread CTAs fused into one (same register cap)
-template <int DP> constexpr int walk_threads() { return 256 * walk_minb<DP>(); }
-static int walk_threads_rt(int DP) { return DP <= 8 ? 768 : (DP <= 16 ? 512 : 256); }
+// Threads per CTA (one CTA per SM): as many warps as the register need of each row width
+// allows — DP <= 8: 1024 (64 registers), 16: 512 (128), 32: 384 (168), 64: 256 (255); measured
+// on B200 against 768 / 640 / 512 (DP 8) and 256 / 320 / 448 / 512 (DP 32), DESIGN.md §6.
+#ifndef KM_WALK_T8
+#define KM_WALK_T8 1024
+#endif
+#ifndef KM_WALK_T16
+#define KM_WALK_T16 512
+#endif
+#ifndef KM_WALK_T32
+#define KM_WALK_T32 384
+#endif
+__host__ __device__ constexpr int walk_threads_of(int DP)
+{
+    return DP <= 8 ? KM_WALK_T8 : (DP <= 16 ? KM_WALK_T16 : (DP <= 32 ? KM_WALK_T32 : 256));
+}
+template <int DP> constexpr int walk_threads() { return walk_threads_of(DP); }
+static int walk_threads_rt(int DP) { return walk_threads_of(DP); }
 
 template <int DP, bool CSMEM, int R, int NH, bool HSMEM>
 __global__ void __launch_bounds__(walk_threads<DP>(), 1)
