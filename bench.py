@@ -286,17 +286,22 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nccl_id, n_global=n,
                      device=local_rank)
+        t1 = time.perf_counter()
         for _ in range(total_iters):
             km2.iterate()
+        t2 = time.perf_counter()
         km2.assignments(out=a_out)
         C_out = km2.centroids()
         t_e2e = time.perf_counter() - t0
+        phases = {"create_ms": 1e3 * (t1 - t0), "iterate_ms": 1e3 * (t2 - t1),
+                  "d2h_ms": 1e3 * (t0 + t_e2e - t2)}
         km2.close()
         t_e2e = max_over_ranks(t_e2e)
         line["e2e"] = {"value": total_iters / t_e2e, "unit": "iters/s",
                        "h2d_bytes_per_step": (hi - lo) * d * 4 / total_iters,
                        "d2h_bytes_per_step": ((hi - lo) * 4 + C_out.nbytes) / total_iters,
-                       "iterations": total_iters, "includes": "create(H2D) + all iterations + D2H a, C"}
+                       "iterations": total_iters, "includes": "create(H2D) + all iterations + D2H a, C",
+                       "phases": phases}
         del Xh
     # ---- CPU baseline: the oracle on the host cores (rank 0, N=1 only) ------------------------
     if world == 1 and not args.no_cpu_baseline:

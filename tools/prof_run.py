@@ -22,15 +22,19 @@ ap.add_argument("--n", type=int, default=8_000_000)
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--engine", default="auto")
 ap.add_argument("--resort", default="auto")
+ap.add_argument("--resort-fraction", type=float, default=0.0)
 args = ap.parse_args()
 X, idx, _ = make_config(args.config, n=args.n)
 C0 = X[idx].astype(np.float64)
 Xd = torch.from_numpy(X).cuda()
-with KMeans(Xd, C0, prune="mti", engine=args.engine, resort=args.resort) as km:
+with KMeans(Xd, C0, prune="mti", engine=args.engine, resort=args.resort,
+            resort_fraction=args.resort_fraction) as km:
     for _ in range(args.iters):
         km.iterate()
     torch.cuda.synchronize()
-    for i, s in enumerate(km.stats()):
+    st = km.stats()
+    print(f"sum ms_iter t=4..{len(st)}: {sum(s['ms_iter'] for s in st[3:]):.3f}")
+    for i, s in enumerate(st):
         print(f"t={i + 1} ms_assign={s['ms_assign']:.3f} ms_iter={s['ms_iter']:.3f} ms_sort={s['ms_sort']:.3f} "
               f"changed={s['changed']} dists={s['dists']} clause1={s['clause1']} refined={s['refined']} "
               f"steps={s['walk_steps']} resorted={s['resorted']}")
