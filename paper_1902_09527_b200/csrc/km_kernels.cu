@@ -550,6 +550,19 @@ __global__ void k_scan_buckets(SortParams p)    // one CTA
 // Rows of a warp that go to the same bucket take consecutive slots (one smem atomic per bucket
 // group, __match_any_sync), so a nearly sorted input is written back in coalesced runs.  Each
 // warp handles G groups of 32 rows per step with all loads issued first (memory parallelism).
+// 32-byte global load / store (LDG/STG.E.ENL2.256): one transaction per 8-float row segment
+__device__ __forceinline__ void ld256(const float4 *src, float4 &a, float4 &b)
+{
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(src));
+}
+__device__ __forceinline__ void st256(float4 *dst, const float4 &a, const float4 &b)
+{
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(dst), "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                 : "memory");
+}
+
 template <int DP>
 __global__ void __launch_bounds__(512) k_scatter(SortParams p)
 {
@@ -573,8 +586,13 @@ __global__ void __launch_bounds__(512) k_scatter(SortParams p)
             const bool v = r < r1;
             key[g] = v ? __ldg(p.keys + r) : 0xffffffffu;
             const float4 *src = reinterpret_cast<const float4 *>(p.X + (v ? r : r0) * DP);
+            if constexpr (DP >= 8) {
 #pragma unroll
-            for (int j = 0; j < DP / 4; ++j) xv[g][j] = __ldg(src + j);
+                for (int j = 0; j < DP / 4; j += 2) ld256(src + j, xv[g][j], xv[g][j + 1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < DP / 4; ++j) xv[g][j] = __ldg(src + j);
+            }
             av[g] = __ldg(p.a + (v ? r : r0));
             uv[g] = __ldg(p.u + (v ? r : r0));
             pv[g] = __ldg(p.perm + (v ? r : r0));
@@ -590,8 +608,13 @@ __global__ void __launch_bounds__(512) k_scatter(SortParams p)
             if (!v) continue;
             const int64_t dst = base + __popc(grp & ((1u << lane) - 1u));
             float4 *dx = reinterpret_cast<float4 *>(p.X2 + dst * DP);
+            if constexpr (DP >= 8) {
 #pragma unroll
-            for (int j = 0; j < DP / 4; ++j) dx[j] = xv[g][j];
+                for (int j = 0; j < DP / 4; j += 2) st256(dx + j, xv[g][j], xv[g][j + 1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < DP / 4; ++j) dx[j] = xv[g][j];
+            }
             p.a2[dst] = av[g];
             p.u2[dst] = uv[g];
             p.perm2[dst] = pv[g];
