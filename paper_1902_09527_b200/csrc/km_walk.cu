@@ -32,6 +32,12 @@ namespace km {
 
 // One CTA per SM: the shared H rows and C are held once per SM rather than once per CTA, which
 // leaves most of the 256 KB L1/shared array as L1 for the candidate tables (walk_threads below).
+#ifndef KM_WALK_R32
+#define KM_WALK_R32 2           // rows per lane at d = 32
+#endif
+#ifndef KM_WALK_HALVES
+#define KM_WALK_HALVES 1        // d >= 32: consume each candidate pair block in two halves
+#endif
 constexpr int kWalkChunk = 256;        // rows a warp claims per work-counter fetch
 constexpr int kQueue = 64;             // mover-queue entries per warp (< 32 left + 32 new)
 
@@ -350,22 +356,45 @@ k_walk(AssignParams p)
 #pragma unroll
             for (int i = 0; i < R; ++i) { m1[i] = 0x7fffffff; m2[i] = 0x7fffffff; }
             for (int j = 0; j < pm; j += 2) {
-                float4 v[DP / 2];
-                if constexpr (DP >= 32) {   // halves the load instructions where they dominate
-#pragma unroll
-                    for (int e = 0; e < DP / 2; e += 2)
-                        ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e, v[e], v[e + 1]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < DP / 2; ++e) v[e] = __ldg(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e);
-                }
                 const float2 cc = __ldg(ccA + (j >> 1));
+                float2 q[R];
+                if constexpr (DP >= 32 && KM_WALK_HALVES && HSMEM) {   // (measured: +2 % on C4, -3.5 % on C5)
+                    // wide rows: the pair block is consumed in two halves of DP/2 coordinates, so
+                    // only DP/4 float4 of it are live at once (registers bound the resident warps)
+#pragma unroll
+                    for (int i = 0; i < R; ++i) q[i] = add2s(xx[i], cc);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        float4 v[DP / 4];
+#pragma unroll
+                        for (int e = 0; e < DP / 4; e += 2)
+                            ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + h * (DP / 4) + e, v[e], v[e + 1]);
+#pragma unroll
+                        for (int i = 0; i < R; ++i)
+#pragma unroll
+                            for (int e = 0; e < DP / 4; ++e) {
+                                q[i] = fma2s(xc[i][h * (DP / 2) + 2 * e], make_float2(v[e].x, v[e].y), q[i]);
+                                q[i] = fma2s(xc[i][h * (DP / 2) + 2 * e + 1], make_float2(v[e].z, v[e].w), q[i]);
+                            }
+                    }
+                } else {
+                    float4 v[DP / 2];
+                    if constexpr (DP >= 32) {   // halves the load instructions where they dominate
+#pragma unroll
+                        for (int e = 0; e < DP / 2; e += 2)
+                            ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e, v[e], v[e + 1]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < DP / 2; ++e) v[e] = __ldg(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e);
+                    }
+#pragma unroll
+                    for (int i = 0; i < R; ++i) q[i] = q_pair<DP>(xc[i], xx[i], cc, v);
+                }
 #pragma unroll
                 for (int i = 0; i < R; ++i) {
-                    const float2 q = q_pair<DP>(xc[i], xx[i], cc, v);
                     int k0, k1;
-                    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(k0) : "r"(__float_as_uint(q.x)), "r"(kmask), "r"(j));
-                    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(k1) : "r"(__float_as_uint(q.y)), "r"(kmask), "r"(j + 1));
+                    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(k0) : "r"(__float_as_uint(q[i].x)), "r"(kmask), "r"(j));
+                    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(k1) : "r"(__float_as_uint(q[i].y)), "r"(kmask), "r"(j + 1));
                     const int lo2 = min(k0, k1), hi2 = max(k0, k1);
                     m2[i] = min(min(max(m1[i], lo2), m2[i]), hi2);
                     m1[i] = min(m1[i], lo2);
@@ -584,14 +613,14 @@ cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, 
 
 size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem)
 {
-    const int R = DP <= 32 ? 2 : 1;
+    const int R = DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1);
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
            (size_t)(walk_threads_rt(DP) / 32) * (32 * R * (DP + 2) + 3 * kQueue) * sizeof(float);
 }
 
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
-template <int DP> constexpr int walk_r() { return DP <= 32 ? 2 : 1; }
+template <int DP> constexpr int walk_r() { return DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1); }
 
 typedef void (*walk_kernel_t)(AssignParams);
 
