@@ -283,3 +283,45 @@ def test_c3_full_size_free_running_and_sampled():
     C_means, _ = oracle.update(sums, counts, Cused)
     assert centroid_rel_err(km.centroids(), C_means).max() <= 1e-12
     km.close()
+
+
+def _full_size_sampled(cfg, shape, warm_iters, sample_n, seed):
+    """Full BASELINE size through the bench's engine and launch configuration: after warm_iters
+    free-running passes, one more pass is checked on a row sample against the fp64 brute-force
+    argmin over the centroids that pass used (near-ties excluded, but none expected), and the
+    resulting centroids against the oracle's means of the GPU's full assignment vector."""
+    X, idx, spec = make_config(cfg)
+    assert X.shape == shape
+    k = spec["k"]
+    C0 = X[idx].astype(float)
+    Xd = torch.from_numpy(X).cuda()
+    km = KMeans(Xd, C0, prune="mti")
+    assert km.engine == "k_walk"
+    for _ in range(warm_iters):
+        km.iterate()
+    Cused = km.centroids()
+    km.iterate()
+    a = km.assignments()
+    st = km.stats()[-1]
+    rng = np.random.default_rng(seed)
+    sample = np.sort(rng.choice(X.shape[0], sample_n, replace=False))
+    a_o, d1, d2 = oracle.assign_brute(X[sample], Cused)
+    ok = ~near_tie_mask(d1, d2)
+    assert np.array_equal(a[sample][ok], a_o[ok])
+    assert int((a[sample] != a_o).sum()) == 0
+    sums, counts = oracle.cluster_sums(X, a, k)
+    C_means, _ = oracle.update(sums, counts, Cused)
+    assert centroid_rel_err(km.centroids(), C_means).max() <= 1e-12
+    # the MTI distance count of the pass: 1 + |S| per non-skipped row, at most n*k
+    assert 0 < st["dists"] <= X.shape[0] * k and st["clause1"] <= X.shape[0]
+    km.close()
+
+
+def test_c4_full_size_sampled():
+    """C4 at full size (n = 65,608,366, d = 32, k = 100)."""
+    _full_size_sampled("c4", (65_608_366, 32), 5, 200_000, 11)
+
+
+def test_c5_full_size_sampled():
+    """C5 at full size (n = 100,000,000, d = 32, k = 1000: H rows in global memory)."""
+    _full_size_sampled("c5", (100_000_000, 32), 4, 50_000, 13)
