@@ -204,8 +204,10 @@ k_walk(AssignParams p)
     const float kappa = 2.f * (2.f * DP + 20.f) * 5.9604645e-8f;
     constexpr int kRows = 32 * R;                   // rows per warp batch
 
-    unsigned long long c_changed = 0, c_dists = 0, c_clause1 = 0, c_refined = 0, c_fb = 0;
-    unsigned long long steps = 0;
+    // per-lane counters: 32 bits (a lane's rows and walk steps stay far below 2^32; registers
+    // are what bounds the resident warps), widened for the warp reduction at the end
+    unsigned long long c_dists = 0;
+    unsigned c_changed32 = 0, c_clause132 = 0, c_refined32 = 0, c_fb32 = 0, steps32 = 0;
 
     constexpr int kBatches = kWalkChunk / kRows;
     auto claim = [&]() -> int {
@@ -282,7 +284,7 @@ k_walk(AssignParams p)
             uu[i] = valid[i] ? __fadd_ru(uold, sF[aold[i]]) : 0.f;          // u += f(a)
             const bool c1 = valid[i] && uu[i] <= sS[aold[i]];                  // clause 1
             active[i] = valid[i] && !c1;
-            c_clause1 += c1;
+            c_clause132 += c1;
             amask |= __ballot_sync(kFull, active[i]) ? (1u << i) : 0u;
         }
         __syncwarp();
@@ -400,7 +402,7 @@ k_walk(AssignParams p)
                     m1[i] = min(m1[i], lo2);
                 }
             }
-            steps += (unsigned long long)pm;
+            steps32 += (unsigned)pm;
             // prefix max of |c'|^2 over the evaluated rows (bounds the error of every key)
             const float cmax = pm > 0 ? __ldg(p.Wmeta + (int64_t)A * kp + ((pm + 1) & ~1) - 1).x : 0.f;
             const float2 *mA = p.Wmeta + (int64_t)A * kp;
@@ -476,7 +478,7 @@ k_walk(AssignParams p)
                     }
                 }
                 if (fallback) {
-                    ++c_fb;
+                    ++c_fb32;
                     const uint64_t *nl = p.NL + (int64_t)aold[i] * p.ks;
                     float xr[DP];
                     {
@@ -501,7 +503,7 @@ k_walk(AssignParams p)
                     const float ub = upper_d(bq, p.g_up, eps);
                     if (q2 < INFINITY && lower_d(q2, p.g_dn, eps) <= ub) {
                         anew[i] = refine64(p.X + (size_t)(row0 + 32 * i + lane) * DP, p.d, p.C64, k, aold[i], nl, ut[i], &unew[i]);
-                        ++c_refined;
+                        ++c_refined32;
                     } else {
                         anew[i] = bc;
                         unew[i] = ub;
@@ -537,7 +539,7 @@ k_walk(AssignParams p)
                 const bool mv = valid[i] && anew[i] != aold[i];
                 const unsigned mm = __ballot_sync(kFull, mv);
                 if (mm) {
-                    c_changed += mv;
+                    c_changed32 += mv;
                     if (mv) {
                         const int slot = mq + __popc(mm & ((1u << lane) - 1u));
                         sQ[slot] = rb + lane; sQ[kQueue + slot] = aold[i]; sQ[2 * kQueue + slot] = anew[i];
@@ -549,6 +551,8 @@ k_walk(AssignParams p)
         }
     }
     flush_moves();
+    unsigned long long c_changed = c_changed32, c_clause1 = c_clause132, c_refined = c_refined32,
+                       c_fb = c_fb32, steps = steps32;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         c_changed += __shfl_xor_sync(kFull, c_changed, o);
