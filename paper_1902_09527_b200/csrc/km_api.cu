@@ -129,7 +129,8 @@ struct km_ctx {
     int32_t *perm[2] = {nullptr, nullptr};
     int cur = 0;
     // sort scratch
-    uint32_t *keys = nullptr, *hist = nullptr, *totals = nullptr, *base = nullptr;
+    uint32_t *keys = nullptr, *hist = nullptr, *totals = nullptr, *base = nullptr, *lohist = nullptr;
+    int32_t *qmap = nullptr;
     int Q = 1, NB = 0, ntiles = 0, tile_rows = 32768;
     int ks = 0;                     // NL row stride
     // centroid state
@@ -170,6 +171,7 @@ struct km_ctx {
     float g_up = 1.f, g_dn = 1.f;
     int t = 0;
     int64_t changed_since_sort = 0;
+    int last_sort_t = 0;            // iteration of the last re-bucketing
     int resort_policy = KM_RESORT_AUTO;
     float resort_fraction = 0.10f;
     std::vector<km_iter_stats> stats;
@@ -282,6 +284,8 @@ km_status resort(km_ctx *c)
     p.X2 = c->X[nw]; p.a2 = c->a[nw]; p.u2 = c->u[nw]; p.perm2 = c->perm[nw];
     p.keys = c->keys; p.hist = c->hist; p.totals = c->totals; p.base = c->base;
     p.NL = c->NL; p.s = c->s; p.ks = c->ks;
+    p.lohist = getenv("KM_LINEAR_Q") ? nullptr : c->lohist;   // A/B: equal-width classes
+    p.qmap = c->qmap;
     p.n = c->n; p.k = c->k; p.DP = c->DP;
     p.Q = c->prune == KM_PRUNE_MTI ? c->Q : 1;
     p.NB = c->k * p.Q;
@@ -292,6 +296,7 @@ km_status resort(km_ctx *c)
     c->launches += l;
     c->cur = nw;
     c->changed_since_sort = 0;
+    c->last_sort_t = c->t;
     return KM_OK;
 }
 
@@ -337,7 +342,10 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
         bool need = false;
         if (c->resort_policy == KM_RESORT_ALWAYS) need = true;
         else if (c->resort_policy == KM_RESORT_AUTO)
-            need = (double)c->changed_since_sort > (double)c->resort_fraction * (double)c->n;
+            // the bucket keys of iteration 1 come from the Forgy centroids' H; by iteration 3 the
+            // centroids have settled, so the first re-bucketing is never later than t = 3
+            need = (double)c->changed_since_sort > (double)c->resort_fraction * (double)c->n ||
+                   (c->t == 3 && c->last_sort_t == 1 && !getenv("KM_NO_T3_SORT"));
         if (need) {
             KM_TRY(resort(c));
             sorted_now = true;
@@ -407,7 +415,7 @@ void free_all(km_ctx *c)
     for (int i = 0; i < 2; ++i) {
         cudaFree(c->X[i]); cudaFree(c->a[i]); cudaFree(c->u[i]); cudaFree(c->perm[i]);
     }
-    cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base);
+    cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base); cudaFree(c->lohist); cudaFree(c->qmap);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
     cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
     cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part);
@@ -463,13 +471,17 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         KM_CUDA(cudaMemsetAsync(c->a[i], 0, (size_t)c->n_alloc * sizeof(int32_t), c->st));
         KM_CUDA(cudaMemsetAsync(c->u[i], 0, (size_t)c->n_alloc * sizeof(float), c->st));
     }
-    c->Q = std::max(1, std::min(32, 4096 / k));
-    if (const char *e = getenv("KM_Q")) c->Q = std::max(1, std::min(c->Q, atoi(e)));
+    // prefix classes per cluster: up to 32 while k*Q fits the scatter's 48 KB of bucket cursors
+    // (k = 100: 32; k = 1000: 12 classes of equal population)
+    c->Q = std::max(1, std::min(32, 12288 / k));
+    if (const char *e = getenv("KM_Q")) c->Q = std::max(1, std::min(12288 / k, atoi(e)));   // A/B
     const int NBmax = k * c->Q;
     c->ntiles = (int)((n + c->tile_rows - 1) / c->tile_rows);
     KM_TRY(dalloc(&c->keys, (size_t)n));
     KM_TRY(dalloc(&c->hist, (size_t)NBmax * c->ntiles));
     KM_TRY(dalloc(&c->totals, (size_t)NBmax));
+    KM_TRY(dalloc(&c->lohist, (size_t)k + 1));
+    KM_TRY(dalloc(&c->qmap, (size_t)k + 1));
     KM_TRY(dalloc(&c->base, (size_t)NBmax));
     KM_TRY(dalloc(&c->C, (size_t)k * d));
     KM_TRY(dalloc(&c->Cprev, (size_t)k * d));

@@ -622,15 +622,142 @@ __global__ void __launch_bounds__(512) k_scatter(SortParams p)
     }
 }
 
+cudaError_t launch_sort_tail(const SortParams &p, cudaStream_t st, int *launches);
+
+// Quantile prefix classes.  The walk's cost per warp is the largest prefix p in it, so rows are
+// bucketed by p in classes of equal population (not equal width): pass 1 computes p per row and
+// its histogram, one CTA turns the histogram into the class map, pass 2 forms the bucket keys.
+__device__ __forceinline__ int prefix_len(const float *sH, bool hs, int a, float u, const uint64_t *NL, int k, int ks)
+{
+    int lo = 0, hi = k - 1;
+    if (hs) {
+        const float *h = sH + a * k;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (h[mid] < u) lo = mid + 1; else hi = mid;
+        }
+    } else {
+        const uint64_t *nl = NL + (int64_t)a * ks;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (key_h(__ldg(nl + mid)) < u) lo = mid + 1; else hi = mid;
+        }
+    }
+    return lo;
+}
+
+__global__ void k_sort_prefix(SortParams p)   // keys[r] = a << 13 | p, lohist[p] += 1
+{
+    extern __shared__ uint32_t shp[];
+    const int k = p.k;
+    const bool hs = k <= kSortSmemK;
+    uint32_t *lh = shp;                                   // k+1
+    float *sH = reinterpret_cast<float *>(shp + ((k + 4) & ~3));
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) lh[i] = 0;
+    if (hs)
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+            const int c = i / k, j = i % k;
+            sH[i] = j < k - 1 ? key_h(p.NL[(int64_t)c * p.ks + j]) : __int_as_float(0x7fc00000);
+        }
+    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.x * p.tile_rows;
+    int64_t r1 = r0 + p.tile_rows;
+    if (r1 > p.n) r1 = p.n;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        const int a = p.a[r];
+        const int lo = prefix_len(sH, hs, a, p.u[r], p.NL, k, p.ks);
+        p.keys[r] = ((uint32_t)a << 13) | (uint32_t)lo;
+        atomicAdd(&lh[lo], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i <= k; i += blockDim.x)
+        if (lh[i]) atomicAdd(&p.lohist[i], lh[i]);
+}
+
+__global__ void k_sort_qmap(SortParams p)     // one CTA of 1024 threads
+{
+    const int k = p.k, Q = p.Q;
+    __shared__ unsigned long long s_tot;
+    uint32_t carry = 0, tot;
+    // total rows with p >= 1
+    unsigned long long part = 0;
+    for (int i = 1 + threadIdx.x; i <= k; i += blockDim.x) part += p.lohist[i];
+    if (threadIdx.x == 0) s_tot = 0;
+    __syncthreads();
+    atomicAdd(&s_tot, part);
+    __syncthreads();
+    const unsigned long long T1 = s_tot;
+    for (int base = 1; base <= k; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i <= k ? p.lohist[i] : 0;
+        const uint32_t ex = block_excl_scan(v, &tot);
+        if (i <= k) {
+            const unsigned long long cum = (unsigned long long)carry + ex;   // rows with 1 <= p' < i
+            int q = T1 ? (int)((unsigned long long)(Q - 1) * cum / T1) : 0;
+            p.qmap[i] = 1 + min(q, Q - 2);
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) p.qmap[0] = 0;
+}
+
+__global__ void k_sort_keys_q(SortParams p)   // keys[r] = a * Q + qmap[p], per-tile histograms
+{
+    extern __shared__ uint32_t shq[];
+    uint32_t *hst = shq;                                  // NB
+    int *qm = reinterpret_cast<int *>(shq + p.NB);        // k+1
+    for (int b = threadIdx.x; b < p.NB; b += blockDim.x) hst[b] = 0;
+    for (int i = threadIdx.x; i <= p.k; i += blockDim.x) qm[i] = p.qmap[i];
+    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.x * p.tile_rows;
+    int64_t r1 = r0 + p.tile_rows;
+    if (r1 > p.n) r1 = p.n;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        const uint32_t kv = p.keys[r];
+        const uint32_t b = (kv >> 13) * (uint32_t)p.Q + (uint32_t)qm[kv & 8191u];
+        p.keys[r] = b;
+        atomicAdd(&hst[b], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < p.NB; b += blockDim.x)
+        p.hist[(int64_t)b * p.ntiles + blockIdx.x] = hst[b];
+}
+
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches)
 {
-    const size_t sh = (size_t)p.NB * sizeof(uint32_t);   // NB <= 4096 -> <= 16 KB
-    const size_t shk = sh + (p.Q > 1 && p.k <= kSortSmemK ? (size_t)p.k * p.k * sizeof(float) : 0);
+    if (p.Q > 1 && p.k <= kQuantK && p.lohist && p.qmap) {
+        const size_t sp = (size_t)((p.k + 4) & ~3) * sizeof(uint32_t) +
+                          (p.k <= kSortSmemK ? (size_t)p.k * p.k * sizeof(float) : 0);
+        const size_t sq = (size_t)(p.NB + p.k + 1) * sizeof(uint32_t);
+        if (sp > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k_sort_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp);
+            if (e != cudaSuccess) return e;
+        }
+        if (sq > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k_sort_keys_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq);
+            if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaMemsetAsync(p.lohist, 0, (size_t)(p.k + 1) * sizeof(uint32_t), st);
+        if (e != cudaSuccess) return e;
+        k_sort_prefix<<<p.ntiles, 512, sp, st>>>(p);
+        k_sort_qmap<<<1, 1024, 0, st>>>(p);
+        k_sort_keys_q<<<p.ntiles, 512, sq, st>>>(p);
+        if (launches) *launches += 3;
+        return launch_sort_tail(p, st, launches);
+    }
+    const size_t shk = (size_t)p.NB * sizeof(uint32_t) + (p.Q > 1 && p.k <= kSortSmemK ? (size_t)p.k * p.k * sizeof(float) : 0);
     if (shk > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_sort_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shk);
         if (e != cudaSuccess) return e;
     }
     k_sort_keys<<<p.ntiles, 512, shk, st>>>(p);
+    if (launches) *launches += 1;
+    return launch_sort_tail(p, st, launches);
+}
+
+cudaError_t launch_sort_tail(const SortParams &p, cudaStream_t st, int *launches)
+{
+    const size_t sh = (size_t)p.NB * sizeof(uint32_t);   // NB <= 12288 -> <= 48 KB
     k_scan_tiles<<<p.NB, 1024, 0, st>>>(p);
     k_scan_buckets<<<1, 1024, 0, st>>>(p);
     switch (p.DP) {
@@ -641,7 +768,7 @@ cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches)
     case 64: k_scatter<64><<<p.ntiles, 512, sh, st>>>(p); break;
     default: return cudaErrorInvalidValue;
     }
-    if (launches) *launches += 4;
+    if (launches) *launches += 3;
     return cudaGetLastError();
 }
 

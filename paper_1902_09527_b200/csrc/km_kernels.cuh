@@ -87,10 +87,13 @@ struct SortParams {
     uint32_t *totals;      // NB
     uint32_t *base;        // NB
     const uint64_t *NL; const float *s;
+    uint32_t *lohist;      // k+1 counts of the prefix length p (quantile classes, k <= kQuantK)
+    int32_t *qmap;         // k+1: p -> class (0 for p = 0, then Q-1 classes of equal population)
     int64_t n;
     int32_t ks;
     int32_t k, DP, Q, NB, ntiles, tile_rows;
 };
+constexpr int kQuantK = 8192;   // quantile prefix classes for k <= this (p packed in 13 bits)
 
 // ---- launchers (km_kernels.cu) ----------------------------------------------------------
 cudaError_t launch_prep(const PrepParams &p, cudaStream_t st);
