@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--prune", default="mti", choices=["mti", "none"])
+    ap.add_argument("--algo", default="kmeans", choices=["kmeans", "skmeans"],
+                    help="skmeans: spherical k-means (PAPER.md §4.2) on the same engine")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -120,23 +122,28 @@ def traffic_from_profile(cfg: str, prune: str, kernel: str):
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_oracle_rate(X, C0, n_full: int, k: int, sample_rows: int, iters: int):
+def cpu_oracle_rate(X, C0, n_full: int, k: int, sample_rows: int, iters: int, spherical: bool = False):
     """The fp64 oracle (oracle/, as it stands) on the first ``sample_rows`` rows: iteration 1
     brute force untimed, then ``iters`` timed MTI iterations (oracle_mti_pass + block sums +
     update).  Returns (full-workload iterations/s extrapolated by rows, seconds, threads)."""
     import numpy as np
     import oracle
     Xs = np.ascontiguousarray(X[:sample_rows])
+    if spherical:   # sk-means: the oracle's projection and re-normalised update
+        Xs, C0 = oracle.normalize_rows(Xs), oracle.normalize_centroids(C0)
+    renorm = (lambda Cm, cnt, Cold: oracle.renormalize(Cm, cnt, Cold)) if spherical else (lambda Cm, cnt, Cold: Cm)
     a, d1, _ = oracle.assign_brute(Xs, C0)
     u = np.sqrt(d1)
     sums, counts = oracle.cluster_sums(Xs, a, k)
     C, _ = oracle.update(sums, counts, C0)
+    C = renorm(C, counts, C0)
     Cprev = C0
     t0 = time.perf_counter()
     for _ in range(iters):
         a, u, _, _, _ = oracle.mti_pass(Xs, C, Cprev, a, u)
         sums, counts = oracle.cluster_sums(Xs, a, k)
         Cprev, (C, _) = C, oracle.update(sums, counts, C)
+        C = renorm(C, counts, Cprev)
     dt = time.perf_counter() - t0
     rate = iters / dt * (sample_rows / n_full)
     return rate, dt, oracle.num_threads()
@@ -154,14 +161,15 @@ def run_reference(args, rank, world):
     if spec.k >= 1000:
         sample = min(spec.n, 200_000)
     # warm-up steps (untimed) then K timed oracle MTI iterations on the sample
-    cpu_oracle_rate(X, C0, spec.n, spec.k, sample, max(1, args.warmup))
-    rate, dt, cores = cpu_oracle_rate(X, C0, spec.n, spec.k, sample, args.steps)
+    sph = args.algo == "skmeans"
+    cpu_oracle_rate(X, C0, spec.n, spec.k, sample, max(1, args.warmup), sph)
+    rate, dt, cores = cpu_oracle_rate(X, C0, spec.n, spec.k, sample, args.steps, sph)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8(d) recipe, seed 0)",
-        "config": {"workload": f"{args.config}: n={spec.n}, d={spec.d}, k={spec.k}", "prune": "mti",
+        "config": {"workload": f"{args.config}: n={spec.n}, d={spec.d}, k={spec.k}", "algo": args.algo, "prune": "mti",
                    "parallelism": "host cores (OpenMP)"},
         "effective_dists_per_s": rate * spec.n * spec.k,
         "cpu_baseline": {"value": rate, "unit": "iters/s", "cores": cores, "kind": "oracle",
@@ -212,6 +220,7 @@ def run_ours(args, rank, world, local_rank):
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
     stream = torch.cuda.current_stream()
     km = KMeans(Xd, C0, prune=args.prune, stream=stream.cuda_stream, rank=rank, world=world,
+                spherical=args.algo == "skmeans",
                 nccl_id=nccl_id, n_global=n)
     for _ in range(args.warmup):
         km.iterate()
@@ -256,13 +265,13 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (SURVEY §8(d) recipe, seed 0; stands in for Friendster-8)",
         "config": {"workload": f"{args.config}: n={n}, d={d}, k={k}, Forgy init, iterations "
                                f"{args.warmup + 1}..{args.warmup + args.steps}",
-                   "prune": args.prune, "parallelism": f"rows sharded over {world} GPU(s)",
+                   "algo": args.algo, "prune": args.prune, "parallelism": f"rows sharded over {world} GPU(s)",
                    "l2": f"inputs {n * 4 * d / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "effective_dists_per_s": iters_per_s * n * k,
         "dists_computed_per_s": dists_computed / (ms_max * 1e-3),
         "hbm_gbs_step": iter_bytes * iters_per_s / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_from_profile(args.config, args.prune, engine),
+                     "frac": achieved / peak, "traffic": traffic_from_profile(args.config, args.prune, engine) if args.algo == "kmeans" else None,
                      "kernel": engine,
                      "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": avg_assign,
                      "peak_source": peak_src},
@@ -285,6 +294,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nccl_id, n_global=n,
+                     spherical=args.algo == "skmeans",
                      device=local_rank)
         t1 = time.perf_counter()
         for _ in range(total_iters):
@@ -309,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
         if k >= 1000:
             sample = min(n, 200_000)
         it = 3
-        rate, dt, cores = cpu_oracle_rate(X, C0, n, k, sample, it)
+        rate, dt, cores = cpu_oracle_rate(X, C0, n, k, sample, it, args.algo == "skmeans")
         line["cpu_baseline"] = {"value": rate, "unit": "iters/s", "cores": cores, "kind": "oracle",
                                 "sample": f"first {sample} rows of {args.config}, {it} MTI iterations "
                                           f"after 1 brute ({dt:.1f} s), extrapolated x{n / sample:.2f} by rows"}

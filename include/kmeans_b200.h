@@ -72,9 +72,15 @@ typedef struct km_options {
     int32_t check_finite;      /* 1 = scan points and centroids for NaN/Inf at create (KM_ENONFINITE) */
     int32_t points_on_host;    /* 1 = points pointer is host memory (pinned preferred); copied at create */
     int32_t resort_policy;     /* KM_RESORT_* */
-    float resort_fraction;     /* AUTO threshold; 0 = default (0.10 CUDA-core engine, 0.5 tensor engine) */
+    float resort_fraction;     /* AUTO threshold; 0 = default (0.25 walk / tensor engines, 0.10 others) */
     int32_t engine;            /* KM_ENGINE_* (default AUTO) */
-    int32_t reserved[7];
+    int32_t spherical;         /* 1 = spherical k-means (§4.2 "sk-means", 1133-1140):
+                                  the context's copy of every row is projected to the unit sphere once
+                                  at create (x / ||x||, fp64, rounded to fp32), the initial centroids
+                                  likewise (fp64), and every update re-normalises the mean (fp64);
+                                  assignment = Euclidean argmin on the sphere = cosine argmax, so MTI
+                                  applies unchanged.  A zero row or zero initial centroid is KM_EARG. */
+    int32_t reserved[6];
 } km_options;
 
 typedef struct km_iter_stats {

@@ -5,3 +5,4 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baselin
 no code.  See ``oracle/kmeans_oracle.c`` for the passages each function follows.
 """
 from .oracle import *  # noqa: F401,F403
+from .skmeans import normalize_centroids, normalize_rows, renormalize, skmeans  # noqa: F401

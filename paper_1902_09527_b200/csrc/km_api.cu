@@ -172,6 +172,7 @@ struct km_ctx {
     int t = 0;
     int64_t changed_since_sort = 0;
     int last_sort_t = 0;            // iteration of the last re-bucketing
+    bool spherical = false;         // sk-means (rows and centroids on the unit sphere)
     int resort_policy = KM_RESORT_AUTO;
     float resort_fraction = 0.10f;
     std::vector<km_iter_stats> stats;
@@ -372,7 +373,8 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     KM_CUDA(cudaEventRecord(ev[4], c->st));
     KM_TRY(allreduce(c));
     KM_CUDA(cudaEventRecord(ev[5], c->st));
-    KM_CUDA(km::launch_update(c->acc, c->S, c->delta_pass ? 1 : 0, c->C, c->Cprev, c->k, c->d, c->DP, c->empty, c->st));
+    KM_CUDA(km::launch_update(c->acc, c->S, c->delta_pass ? 1 : 0, c->C, c->Cprev, c->k, c->d, c->DP, c->empty,
+                              c->spherical ? 1 : 0, c->st));
     c->launches += 1;
     KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, c->st));
@@ -444,6 +446,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     c->n_global = o->n_global > 0 ? o->n_global : n * (int64_t)o->world;
     c->resort_policy = o->resort_policy;
     c->resort_fraction = o->resort_fraction > 0.f ? o->resort_fraction : 0.10f;
+    c->spherical = o->spherical != 0;
     KM_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
     if (o->stream) {
         c->st = static_cast<cudaStream_t>(o->stream);
@@ -518,8 +521,29 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     }
     KM_CUDA(km::launch_iota(c->perm[0], n, c->st));
     c->launches += 1;
+    std::vector<double> C0n;
+    if (c->spherical) {
+        // sk-means: rows onto the unit sphere on the device, initial centroids here (same steps)
+        KM_CUDA(cudaMemsetAsync(c->work, 0, sizeof(int), c->st));
+        KM_CUDA(km::launch_normalize_rows(X0, n, d, DP, c->work, c->st));
+        c->launches += 1;
+        int flag = 0;
+        KM_CUDA(cudaMemcpyAsync(&flag, c->work, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+        KM_CUDA(cudaStreamSynchronize(c->st));
+        if (flag) return fail(KM_EARG, "spherical: a point has zero norm");
+        C0n.assign(C0, C0 + (size_t)k * d);
+        for (int c_ = 0; c_ < k; ++c_) {
+            double ss = 0.0;
+            for (int j = 0; j < d; ++j) ss += C0n[(size_t)c_ * d + j] * C0n[(size_t)c_ * d + j];
+            if (!(ss > 0.0)) return fail(KM_EARG, "spherical: init_centroids row %d has zero norm", c_);
+            const double nrm = std::sqrt(ss);
+            for (int j = 0; j < d; ++j) C0n[(size_t)c_ * d + j] /= nrm;
+        }
+        C0 = C0n.data();
+    }
     KM_CUDA(cudaMemcpyAsync(c->C, C0, (size_t)k * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
     KM_CUDA(cudaMemcpyAsync(c->Cprev, C0, (size_t)k * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    KM_CUDA(cudaStreamSynchronize(c->st));   // C0n is host memory of this scope
     if (o->check_finite) {
         for (int64_t i = 0; i < (int64_t)k * d; ++i)
             if (!std::isfinite(C0[i])) return fail(KM_ENONFINITE, "init_centroids[%lld] is not finite", (long long)i);

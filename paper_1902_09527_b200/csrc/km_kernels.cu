@@ -395,7 +395,7 @@ cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems,
 // S holds the running per-cluster sums | count: delta = 0 -> S = acc (full reduction of this
 // pass), delta = 1 -> S += acc (acc holds only the moves of this pass).
 __global__ void k_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
-                         int DP, int *empty)
+                         int DP, int *empty, int spherical)
 {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;     // one thread per cluster
     if (c >= k) return;
@@ -412,12 +412,26 @@ __global__ void k_update(const double *acc, double *S, int delta, double *C, dou
         Cprev[ci] = old;
         C[ci] = cnt > 0.5 ? v / cnt : old;
     }
+    if (spherical && cnt > 0.5) {
+        // sk-means update: the mean re-normalised to unit length, in the oracle's
+        // order (sequential fp64 sum of squares, correctly rounded sqrt and divisions); a zero mean
+        // keeps the previous centroid
+        double *Cc = C + (int64_t)c * d;
+        double ss = 0.0;
+        for (int j = 0; j < d; ++j) ss = __dadd_rn(ss, __dmul_rn(Cc[j], Cc[j]));
+        if (ss > 0.0) {
+            const double nrm = __dsqrt_rn(ss);
+            for (int j = 0; j < d; ++j) Cc[j] = __ddiv_rn(Cc[j], nrm);
+        } else {
+            for (int j = 0; j < d; ++j) Cc[j] = Cprev[(int64_t)c * d + j];
+        }
+    }
 }
 
 cudaError_t launch_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
-                          int DP, int *empty, cudaStream_t st)
+                          int DP, int *empty, int spherical, cudaStream_t st)
 {
-    k_update<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(acc, S, delta, C, Cprev, k, d, DP, empty);
+    k_update<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(acc, S, delta, C, Cprev, k, d, DP, empty, spherical);
     return cudaGetLastError();
 }
 
@@ -858,6 +872,30 @@ __global__ void k_check_finite(const float *X, int64_t count, int *flag)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x)
         if (!isfinite(X[i])) { *flag = 1; return; }
+}
+
+// sk-means: every row projected to the unit sphere once: x / ||x|| with the
+// squared norm summed sequentially in fp64, a correctly rounded sqrt and division, rounded to
+// fp32 — the oracle's normalize_rows step for step; *flag = 1 if a row has zero norm
+__global__ void k_normalize_rows(float *X, int64_t n, int d, int DP, int *flag)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        float *x = X + r * DP;
+        double ss = 0.0;
+        for (int j = 0; j < d; ++j) {
+            const double v = (double)x[j];
+            ss = __dadd_rn(ss, __dmul_rn(v, v));
+        }
+        if (!(ss > 0.0)) { *flag = 1; continue; }
+        const double nrm = __dsqrt_rn(ss);
+        for (int j = 0; j < d; ++j) x[j] = __double2float_rn(__ddiv_rn((double)x[j], nrm));
+    }
+}
+
+cudaError_t launch_normalize_rows(float *X, int64_t n, int d, int DP, int *flag, cudaStream_t st)
+{
+    k_normalize_rows<<<148 * 8, 256, 0, st>>>(X, n, d, DP, flag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_check_finite(const float *X, int64_t count, int *flag, cudaStream_t st)

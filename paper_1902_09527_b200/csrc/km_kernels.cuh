@@ -119,7 +119,7 @@ int walk_grid(int DP, bool csmem, int k, int kp, bool whs, int num_sms);
 cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int kp, int whs,
                              float4 *Wblk, float *Wcc, float2 *Wmeta, float *WH, cudaStream_t st);
 cudaError_t launch_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
-                          int DP, int *empty, cudaStream_t st);
+                          int DP, int *empty, int spherical, cudaStream_t st);
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches);
 cudaError_t launch_sse(const float *X, const int32_t *a, const double *C, int64_t n, int d,
                        int DP, double *out, cudaStream_t st);
@@ -128,5 +128,6 @@ cudaError_t launch_unpermute(const int32_t *a, const int32_t *perm, int64_t n, i
 cudaError_t launch_iota(int32_t *perm, int64_t n, cudaStream_t st);
 cudaError_t launch_pad_rows(const float *X, float *Xp, int64_t n, int d, int DP, cudaStream_t st);
 cudaError_t launch_check_finite(const float *X, int64_t count, int *flag, cudaStream_t st);
+cudaError_t launch_normalize_rows(float *X, int64_t n, int d, int DP, int *flag, cudaStream_t st);
 
 }  // namespace km

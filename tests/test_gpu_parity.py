@@ -325,3 +325,28 @@ def test_c4_full_size_sampled():
 def test_c5_full_size_sampled():
     """C5 at full size (n = 100,000,000, d = 32, k = 1000: H rows in global memory)."""
     _full_size_sampled("c5", (100_000_000, 32), 4, 50_000, 13)
+
+
+# ---- spherical k-means (SURVEY §8(f) NEXT-4; PAPER.md §4.2 lines 1133-1140) -------------------
+@pytest.mark.parametrize("cfg,n", [("c1", None), ("c2", None), ("c3", 1_000_000)])
+def test_skmeans_free_running(cfg, n):
+    """sk-means through the same MTI engine: rows and centroids on the unit sphere (exact-mode
+    arithmetic of the normalisation matches the oracle's step for step); strict parity."""
+    X, idx, spec = make_config(cfg, n=n)
+    C0 = X[idx].astype(float)
+    iters = 30 if cfg != "c1" else 100
+    r = oracle.skmeans(X, C0, iters, 0)
+    g = gpu_run(X, C0, iters, "mti", spherical=True)
+    assert g["iterations"] == r.iterations
+    assert np.array_equal(g["a"], r.a), int((g["a"] != r.a).sum())
+    assert centroid_rel_err(g["C"], r.C).max() <= 1e-12
+    assert np.allclose(np.linalg.norm(g["C"], axis=1), 1.0, rtol=0, atol=1e-12)
+    assert [s["changed"] for s in g["stats"]] == r.changed.tolist()
+    assert abs(g["sse"] - r.final_sse) <= 1e-10 * r.final_sse
+
+
+def test_skmeans_zero_row_rejected():
+    X = np.array([[1, 0], [0, 0], [0, 2]], np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    with pytest.raises(KMeansError):
+        KMeans(Xd, X[[0, 2]].astype(float), spherical=True)
