@@ -155,6 +155,19 @@ km_status kmeans_sse(km_ctx *ctx, double *out);
 /* Copy up to cap per-iteration records (oldest first); *count = records available. */
 km_status kmeans_get_stats(km_ctx *ctx, km_iter_stats *out, int32_t cap, int32_t *count);
 
+/* k-means++ D^2 seeding (§4.3, Eq. 2).
+ * points: n x d fp32 row-major, device memory of `device` (borrowed) or host memory when
+ * points_on_host = 1 (copied).  c_1 = row first_index; c_m (m = 2..k) = the row drawn with
+ * probability D(x)^2 / sum D^2 using the caller's uniforms[m-2] in [0,1) (k-1 values, host).
+ * The draw is exact and reproducible (reading B9): D^2 in fp64 summed in coordinate
+ * order, sum D^2 over fixed 65536-row blocks in order, first row whose running sum exceeds
+ * u * sum.  Outputs (host, caller-owned): chosen[k] row indices, centroids k x d fp64 (the
+ * chosen rows).  Errors: KM_EARG (sizes, NULLs, first_index out of range, uniforms outside
+ * [0,1), fewer than k distinct rows), KM_ECUDA, KM_ENOMEM.  stream: cudaStream_t or NULL. */
+km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *points, int32_t points_on_host,
+                               int64_t first_index, const double *uniforms, int32_t device, void *stream,
+                               int64_t *chosen, double *centroids);
+
 /* Number of kernel launches this context has issued so far (for launch accounting). */
 int64_t kmeans_launch_count(const km_ctx *ctx);
 

@@ -52,6 +52,9 @@ SIGNATURES = {
     "kmeans_sse": (ct.c_int32, [ct.c_void_p, ct.POINTER(ct.c_double)]),
     "kmeans_get_stats": (ct.c_int32, [ct.c_void_p, ct.POINTER(KmIterStats), ct.c_int32,
                                       ct.POINTER(ct.c_int32)]),
+    "kmeans_seed_plusplus": (ct.c_int32, [ct.c_int64, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_int32,
+                                          ct.c_int64, ct.c_void_p, ct.c_int32, ct.c_void_p, ct.c_void_p,
+                                          ct.c_void_p]),
     "kmeans_launch_count": (ct.c_int64, [ct.c_void_p]),
     "kmeans_engine": (ct.c_char_p, [ct.c_void_p]),
     "kmeans_destroy": (None, [ct.c_void_p]),

@@ -800,4 +800,54 @@ const char *kmeans_last_error(void) { return g_err.c_str(); }
 
 const char *kmeans_version(void) { return "kmeans_b200 0.1.0 (sm_100a)"; }
 
+km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *points, int32_t points_on_host,
+                               int64_t first_index, const double *uniforms, int32_t device, void *stream,
+                               int64_t *chosen, double *centroids)
+{
+    g_err.clear();
+    if (n < 1 || d < 1 || k < 1 || k > n) return fail(KM_EARG, "n=%lld d=%d k=%d", (long long)n, d, k);
+    if (!points || !chosen || !centroids || (k > 1 && !uniforms)) return fail(KM_EARG, "NULL argument");
+    if (first_index < 0 || first_index >= n) return fail(KM_EARG, "first_index=%lld", (long long)first_index);
+    for (int m = 0; m + 1 < k; ++m)
+        if (!(uniforms[m] >= 0.0 && uniforms[m] < 1.0)) return fail(KM_EARG, "uniforms[%d] not in [0,1)", m);
+    KM_CUDA(cudaSetDevice(device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    float *Xd = nullptr, *crow = nullptr;
+    double *D2 = nullptr, *bsum = nullptr;
+    int64_t *dsel = nullptr;
+    const int64_t nb = (n + 65535) / 65536;
+    auto cleanup = [&]() {
+        if (points_on_host) cudaFree(Xd);
+        cudaFree(crow); cudaFree(D2); cudaFree(bsum); cudaFree(dsel);
+    };
+    km_status s = KM_OK;
+    do {
+        if (points_on_host) {
+            if ((s = dalloc(&Xd, (size_t)n * d)) != KM_OK) break;
+            if (cudaMemcpyAsync(Xd, points, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+                s = fail(KM_ECUDA, "copy of the points"); break;
+            }
+        } else {
+            Xd = const_cast<float *>(points);
+        }
+        if ((s = dalloc(&crow, (size_t)d)) != KM_OK) break;
+        if ((s = dalloc(&D2, (size_t)n)) != KM_OK) break;
+        if ((s = dalloc(&bsum, (size_t)nb)) != KM_OK) break;
+        if ((s = dalloc(&dsel, (size_t)1)) != KM_OK) break;
+        cudaError_t e = km::seed_plusplus(Xd, n, d, d, k, first_index, uniforms, D2, bsum, crow, dsel, chosen, st);
+        if (e == cudaErrorInvalidValue) { s = fail(KM_EARG, "fewer than k distinct rows"); break; }
+        if (e != cudaSuccess) { s = fail(KM_ECUDA, "seed_plusplus: %s", cudaGetErrorString(e)); break; }
+        std::vector<float> row((size_t)d);
+        for (int m = 0; m < k; ++m) {
+            if (cudaMemcpy(row.data(), Xd + chosen[m] * d, (size_t)d * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+                s = fail(KM_ECUDA, "copy of a chosen row"); break;
+            }
+            for (int j = 0; j < d; ++j) centroids[(size_t)m * d + j] = (double)row[j];
+        }
+    } while (false);
+    cudaStreamSynchronize(st);
+    cleanup();
+    return s;
+}
+
 }  // extern "C"

@@ -158,3 +158,41 @@ class KMeans:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def seed_plusplus(points, k: int, uniforms, first_index: int, *, device: Optional[int] = None, stream=None):
+    """k-means++ D² seeding (Eq. 2) through ``kmeans_seed_plusplus``: returns
+    (chosen int64[k] row indices, centroids fp64 k x d).  ``uniforms``: k-1 draws in [0,1)."""
+    L = C.lib()
+    on_host = 1
+    dev = 0 if device is None else device
+    try:
+        import torch
+        if isinstance(points, torch.Tensor):
+            if points.dtype != torch.float32 or not points.is_contiguous():
+                raise ValueError("points must be a contiguous float32 tensor")
+            if points.is_cuda:
+                on_host = 0
+                dev = points.device.index if device is None else device
+                if stream is None:
+                    stream = torch.cuda.current_stream(dev).cuda_stream
+            else:
+                points = points.numpy()
+    except ImportError:
+        pass
+    if on_host:
+        points = np.ascontiguousarray(points, dtype=np.float32)
+        ptr = points.ctypes.data
+    else:
+        ptr = points.data_ptr()
+    n, d = points.shape
+    u = np.ascontiguousarray(uniforms, dtype=np.float64).reshape(-1)
+    if u.size < k - 1:
+        raise ValueError("need k-1 uniforms")
+    chosen = np.empty(k, np.int64)
+    cent = np.empty((k, d), np.float64)
+    C.check(L.kmeans_seed_plusplus(int(n), int(d), int(k), ct.c_void_p(ptr), on_host, int(first_index),
+                                   ct.c_void_p(u.ctypes.data), int(dev),
+                                   ct.c_void_p(int(stream) if stream is not None else 0),
+                                   ct.c_void_p(chosen.ctypes.data), ct.c_void_p(cent.ctypes.data)))
+    return chosen, cent

@@ -350,3 +350,34 @@ def test_skmeans_zero_row_rejected():
     Xd = torch.from_numpy(X).cuda()
     with pytest.raises(KMeansError):
         KMeans(Xd, X[[0, 2]].astype(float), spherical=True)
+
+
+# ---- k-means++ D² seeding (Eq. 2) ---------------------------------
+@pytest.mark.parametrize("cfg,n", [("c1", None), ("c2", None), ("c3", 2_000_000)])
+def test_seed_plusplus_matches_oracle(cfg, n):
+    """The GPU draws the same rows as the oracle for the same uniforms (reading B9), from device
+    and from host memory; the seeded run then matches the oracle's Lloyd from those centroids."""
+    from paper_1902_09527_b200 import seed_plusplus
+    X, _, spec = make_config(cfg, n=n)
+    k = spec["k"]
+    rng = np.random.default_rng(17)
+    u = rng.random(k - 1)
+    first = int(rng.integers(X.shape[0]))
+    ch_o, C_o = oracle.seed_plusplus(X, k, u, first)
+    ch_g, C_g = seed_plusplus(torch.from_numpy(X).cuda(), k, u, first)
+    assert ch_g.tolist() == ch_o.tolist()
+    assert np.array_equal(C_g, C_o)
+    ch_h, _ = seed_plusplus(X, k, u, first)
+    assert ch_h.tolist() == ch_o.tolist()
+    if cfg == "c1":
+        r = oracle.lloyd(X, C_o, 100, 0, "mti")
+        assert_strict(gpu_run(X, C_g, 100), r)
+
+
+def test_seed_plusplus_errors():
+    from paper_1902_09527_b200 import seed_plusplus
+    X = np.ones((4, 3), np.float32)
+    with pytest.raises(KMeansError):
+        seed_plusplus(X, 2, [0.5], 0)            # fewer than k distinct rows
+    with pytest.raises(KMeansError):
+        seed_plusplus(np.eye(3, dtype=np.float32), 2, [1.5], 0)
