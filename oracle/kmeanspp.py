@@ -13,7 +13,8 @@ from __future__ import annotations
 
 import numpy as np
 
-BLOCK = 65536
+BLOCK = 1024        # rows per block
+GROUP = 1024        # blocks per group
 
 
 def d2_to(X64, c):
@@ -25,44 +26,64 @@ def d2_to(X64, c):
     return s
 
 
-def _running_sum(vals):
-    """Running sums of vals in order (np.add.accumulate is a sequential left-to-right loop)."""
-    return np.add.accumulate(vals) if len(vals) else np.zeros(0)
+def _seq_sum(vals):
+    """Left-to-right sum (np.add.accumulate is a sequential loop); 0.0 for an empty list."""
+    return float(np.add.accumulate(vals)[-1]) if len(vals) else 0.0
+
+
+def _first_crossing(vals, t):
+    """Index of the first running sum (left to right) that exceeds t, with that sum's start
+    value; (-1, _) if none."""
+    run = 0.0
+    for i, v in enumerate(vals):
+        nxt = run + v
+        if nxt > t:
+            return i, run
+        run = nxt
+    return -1, run
+
+
+def _last_positive(vals):
+    pos = np.nonzero(np.asarray(vals) > 0.0)[0]
+    return int(pos[-1]) if pos.size else -1
 
 
 def draw(D2, u):
-    """The row drawn for uniform u (reading B9); -1 if every D² is 0."""
+    """The row drawn for uniform u (reading B9); -1 if every D² is 0.
+
+    Order of every sum: rows of a block (BLOCK rows) in row order; blocks of a group (GROUP
+    blocks) in block order; groups in group order.  The target u·total is located by running
+    sums at each level, top-down; where rounding leaves no crossing, the last positive entry."""
     n = D2.shape[0]
     nb = (n + BLOCK - 1) // BLOCK
-    bsum = [float(_running_sum(D2[b * BLOCK:(b + 1) * BLOCK])[-1]) for b in range(nb)]
-    total = 0.0
-    for v in bsum:
-        total = total + v
+    ng = (nb + GROUP - 1) // GROUP
+    bsum = [_seq_sum(D2[b * BLOCK:(b + 1) * BLOCK]) for b in range(nb)]
+    gsum = [_seq_sum(bsum[g * GROUP:(g + 1) * GROUP]) for g in range(ng)]
+    total = _seq_sum(gsum)
     target = u * total
-    R, bs, Rs = 0.0, -1, 0.0
-    for b in range(nb):
-        nxt = R + bsum[b]
-        if nxt > target:
-            bs, Rs = b, R
-            break
-        R = nxt
-    scan = True
-    if bs < 0:                                   # rounding left target >= total
-        scan = False
-        pos = [b for b in range(nb) if bsum[b] > 0.0]
-        if not pos:
+    g, R = _first_crossing(gsum, target)
+    scan = g >= 0
+    if not scan:
+        g = _last_positive(gsum)
+        if g < 0:
             return -1
-        bs = pos[-1]
-    t2 = target - Rs
-    blk = D2[bs * BLOCK:(bs + 1) * BLOCK]
-    run = _running_sum(blk)
-    last = -1
-    for i in range(blk.shape[0]):
-        if blk[i] > 0.0:
-            last = bs * BLOCK + i
-            if scan and run[i] > t2:
-                return bs * BLOCK + i
-    return last
+    gb = bsum[g * GROUP:(g + 1) * GROUP]
+    if scan:
+        t1 = target - R
+        bi, P = _first_crossing(gb, t1)
+        scan = bi >= 0
+    if not scan:
+        bi = _last_positive(gb)
+    b = g * GROUP + bi
+    blk = D2[b * BLOCK:(b + 1) * BLOCK]
+    if scan:
+        t2 = t1 - P
+        run = 0.0
+        for i in range(blk.shape[0]):
+            run = run + blk[i]
+            if blk[i] > 0.0 and run > t2:
+                return b * BLOCK + i
+    return b * BLOCK + _last_positive(blk)
 
 
 def seed_plusplus(X, k, uniforms, first_index):

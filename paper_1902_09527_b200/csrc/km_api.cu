@@ -815,7 +815,7 @@ km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *poi
     float *Xd = nullptr, *crow = nullptr;
     double *D2 = nullptr, *bsum = nullptr;
     int64_t *dsel = nullptr;
-    const int64_t nb = (n + 65535) / 65536;
+    const int64_t nb = (n + 1023) / 1024, ng = (nb + 1023) / 1024;   // km_seed.cu block / group
     auto cleanup = [&]() {
         if (points_on_host) cudaFree(Xd);
         cudaFree(crow); cudaFree(D2); cudaFree(bsum); cudaFree(dsel);
@@ -832,7 +832,7 @@ km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *poi
         }
         if ((s = dalloc(&crow, (size_t)d)) != KM_OK) break;
         if ((s = dalloc(&D2, (size_t)n)) != KM_OK) break;
-        if ((s = dalloc(&bsum, (size_t)nb)) != KM_OK) break;
+        if ((s = dalloc(&bsum, (size_t)(nb + ng))) != KM_OK) break;
         if ((s = dalloc(&dsel, (size_t)1)) != KM_OK) break;
         cudaError_t e = km::seed_plusplus(Xd, n, d, d, k, first_index, uniforms, D2, bsum, crow, dsel, chosen, st);
         if (e == cudaErrorInvalidValue) { s = fail(KM_EARG, "fewer than k distinct rows"); break; }

@@ -42,10 +42,10 @@ def test_draw_law_matches_d2_weights():
 
 
 def test_block_boundaries():
-    """Rows spread over several 65536-row blocks: the draw lands where the cumulative weight
+    """Rows spread over several blocks and groups: the draw lands where the cumulative weight
     crosses u·total (brute-force cumulative sum over all rows)."""
     rng = np.random.default_rng(1)
-    n = 3 * 65536 + 123
+    n = 2 * 1024 * 1024 + 3 * 1024 + 123
     D2 = rng.random(n) ** 4
     tot = np.cumsum(D2)
     for u in [0.0, 0.1, 0.3333, 0.5, 0.77, 0.999999]:
