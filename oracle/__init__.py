@@ -6,4 +6,4 @@ no code.  See ``oracle/kmeans_oracle.c`` for the passages each function follows.
 """
 from .oracle import *  # noqa: F401,F403
 from .skmeans import normalize_centroids, normalize_rows, renormalize, skmeans  # noqa: F401
-from .kmeanspp import seed_plusplus  # noqa: F401
+from .kmeanspp import kmeanspp_multirun, seed_plusplus  # noqa: F401

@@ -98,3 +98,15 @@ def seed_plusplus(X, k, uniforms, first_index):
         chosen.append(i)
         D2 = np.minimum(D2, d2_to(X64, X64[i]))
     return np.array(chosen, np.int64), X64[chosen].copy()
+
+
+def kmeanspp_multirun(X, k, runs, max_iters, tol=0):
+    """PAPER.md §4.3: r seeded runs of Lloyd's, the one with the smallest SSE (earlier on ties)."""
+    from .oracle import lloyd
+    best = None
+    for i, (first, u) in enumerate(runs):
+        _, C0 = seed_plusplus(X, k, u, first)
+        r = lloyd(X, C0, max_iters, tol, "brute")
+        if best is None or r.final_sse < best[3]:
+            best = (i, r.a, r.C, r.final_sse, r.iterations)
+    return best

@@ -196,3 +196,20 @@ def seed_plusplus(points, k: int, uniforms, first_index: int, *, device: Optiona
                                    ct.c_void_p(int(stream) if stream is not None else 0),
                                    ct.c_void_p(chosen.ctypes.data), ct.c_void_p(cent.ctypes.data)))
     return chosen, cent
+
+
+def kmeanspp_multirun(points, k: int, runs, max_iters: int, tol: int = 0, *, prune: str = "mti",
+                      device: Optional[int] = None):
+    """k-means++ as PAPER.md §4.3 describes it (lines 1141-1149): r runs, each seeded by D²
+    sampling (Eq. 2) and refined by Lloyd's (here the MTI engine), keeping the run with the
+    smallest SSE (ties: the earlier run).  ``runs``: a list of (first_index, uniforms[k-1]).
+    Returns (best run index, assignments, centroids, SSE, iterations)."""
+    best = None
+    for i, (first, u) in enumerate(runs):
+        _, C0 = seed_plusplus(points, k, u, first, device=device)
+        with KMeans(points, C0, prune=prune, device=device) as km:
+            it, _ = km.run(max_iters, tol)
+            sse = km.sse()
+            if best is None or sse < best[3]:
+                best = (i, km.assignments(), km.centroids(), sse, it)
+    return best

@@ -381,3 +381,17 @@ def test_seed_plusplus_errors():
         seed_plusplus(X, 2, [0.5], 0)            # fewer than k distinct rows
     with pytest.raises(KMeansError):
         seed_plusplus(np.eye(3, dtype=np.float32), 2, [1.5], 0)
+
+
+def test_kmeanspp_multirun_matches_oracle():
+    """k-means++ with r = 3 runs on C1: same best run, assignments and centroids as the oracle."""
+    from paper_1902_09527_b200 import kmeanspp_multirun
+    X, _, spec = make_config("c1")
+    rng = np.random.default_rng(23)
+    runs = [(int(rng.integers(X.shape[0])), rng.random(spec["k"] - 1)) for _ in range(3)]
+    bo = oracle.kmeanspp_multirun(X, spec["k"], runs, 100)
+    bg = kmeanspp_multirun(torch.from_numpy(X).cuda(), spec["k"], runs, 100)
+    assert bg[0] == bo[0] and bg[4] == bo[4]
+    assert np.array_equal(bg[1], bo[1])
+    assert centroid_rel_err(bg[2], bo[2]).max() <= 1e-12
+    assert abs(bg[3] - bo[3]) <= 1e-12 * bo[3]

@@ -52,3 +52,13 @@ def test_block_boundaries():
         i = oracle.kmeanspp.draw(D2, u)
         j = int(np.searchsorted(tot, u * tot[-1], side="right"))
         assert abs(i - j) <= 1, (u, i, j)       # equal up to fp64 rounding of the two sums
+
+
+def test_multirun_keeps_min_sse():
+    """PAPER.md §4.3: the best of r runs is the one with the minimum SSE."""
+    rng = np.random.default_rng(2)
+    X = np.concatenate([rng.normal(size=(200, 2)) + c for c in ([0, 0], [8, 0], [0, 8])]).astype(np.float32)
+    runs = [(int(rng.integers(600)), rng.random(2)) for _ in range(4)]
+    best = oracle.kmeanspp_multirun(X, 3, runs, 50)
+    sses = [oracle.lloyd(X, oracle.seed_plusplus(X, 3, u, f)[1], 50, 0, "brute").final_sse for f, u in runs]
+    assert best[0] == int(np.argmin(sses)) and best[3] == min(sses)
