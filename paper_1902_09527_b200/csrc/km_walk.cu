@@ -38,7 +38,10 @@ namespace km {
 #ifndef KM_WALK_HALVES
 #define KM_WALK_HALVES 1        // d >= 32: consume each candidate pair block in two halves
 #endif
-constexpr int kWalkChunk = 256;        // rows a warp claims per work-counter fetch
+#ifndef KM_WALK_CHUNK
+#define KM_WALK_CHUNK 128       // measured: 64 1.73 ms, 128 1.67, 256 1.69, 512 1.73, 1024 1.80 (C3)
+#endif
+constexpr int kWalkChunk = KM_WALK_CHUNK;   // rows a warp claims per work-counter fetch
 constexpr int kQueue = 64;             // mover-queue entries per warp (< 32 left + 32 new)
 
 __host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // float4 per candidate pair
