@@ -289,28 +289,35 @@ def run_ours(args, rank, world, local_rank):
         Xh.numpy()[:] = X
         total_iters = args.warmup + args.steps
         a_out = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)   # caller-owned, pinned
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nccl_id, n_global=n,
-                     spherical=args.algo == "skmeans",
-                     device=local_rank)
-        t1 = time.perf_counter()
-        for _ in range(total_iters):
-            km2.iterate()
-        t2 = time.perf_counter()
-        km2.assignments(out=a_out)
-        C_out = km2.centroids()
-        t_e2e = time.perf_counter() - t0
-        phases = {"create_ms": 1e3 * (t1 - t0), "iterate_ms": 1e3 * (t2 - t1),
-                  "d2h_ms": 1e3 * (t0 + t_e2e - t2)}
-        km2.close()
+        # two passes of the whole end-to-end run; the first (untimed) is the e2e warm-up — the first
+        # DMA from a freshly pinned buffer pays a one-time mapping cost (measured: create 140 ms
+        # instead of 45 ms for C3's 2.1 GB)
+        for rep in range(2):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nccl_id, n_global=n,
+                         spherical=args.algo == "skmeans",
+                         device=local_rank)
+            t1 = time.perf_counter()
+            for _ in range(total_iters):
+                km2.iterate()
+            t2 = time.perf_counter()
+            km2.assignments(out=a_out)
+            C_out = km2.centroids()
+            t_e2e = time.perf_counter() - t0
+            phases = {"create_ms": 1e3 * (t1 - t0), "iterate_ms": 1e3 * (t2 - t1),
+                      "d2h_ms": 1e3 * (t0 + t_e2e - t2)}
+            km2.close()
+            if rep == 0:
+                phases_warm = phases
+        phases["warmup_pass"] = phases_warm
         t_e2e = max_over_ranks(t_e2e)
         line["e2e"] = {"value": total_iters / t_e2e, "unit": "iters/s",
                        "h2d_bytes_per_step": (hi - lo) * d * 4 / total_iters,
                        "d2h_bytes_per_step": ((hi - lo) * 4 + C_out.nbytes) / total_iters,
-                       "iterations": total_iters, "includes": "create(H2D) + all iterations + D2H a, C",
+                       "iterations": total_iters, "includes": "create(H2D) + all iterations + D2H a, C (second of two passes)",
                        "phases": phases}
         del Xh
     # ---- CPU baseline: the oracle on the host cores (rank 0, N=1 only) ------------------------
