@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -93,9 +94,9 @@ NcclApi *nccl()
 
 struct HostStat {
     unsigned long long local[8];   // changed, dists, clause1, refined, walk_steps (this rank)
-    unsigned long long global[8];  // after allreduce
-    int empty;
+    int empty;                     // follows the counters in device scratch: one copy for both
     int pad;
+    unsigned long long global[8];  // after allreduce (world 1: = local)
 };
 
 int pad_dim(int d)
@@ -303,11 +304,7 @@ km_status resort(km_ctx *c)
 
 km_status allreduce(km_ctx *c)
 {
-    if (c->world <= 1) {
-        KM_CUDA(cudaMemcpyAsync(c->counters_g, c->counters, 8 * sizeof(unsigned long long),
-                                cudaMemcpyDeviceToDevice, c->st));
-        return KM_OK;
-    }
+    if (c->world <= 1) return KM_OK;   // global counters = local (iterate copies them once)
     NcclApi *N = nccl();
     if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable");
     ncclResult_t r;
@@ -376,14 +373,17 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     KM_CUDA(km::launch_update(c->acc, c->S, c->delta_pass ? 1 : 0, c->C, c->Cprev, c->k, c->d, c->DP, c->empty,
                               c->spherical ? 1 : 0, c->st));
     c->launches += 1;
-    KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long),
+    static_assert(offsetof(HostStat, empty) == 8 * sizeof(unsigned long long), "HostStat layout");
+    // counters[8] and the ints that follow them (empty, ...) in one copy
+    KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long) + 2 * sizeof(int),
                             cudaMemcpyDeviceToHost, c->st));
-    KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 8 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, c->st));
-    KM_CUDA(cudaMemcpyAsync(&c->hstat->empty, c->empty, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    if (c->world > 1)
+        KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 8 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, c->st));
     KM_CUDA(cudaEventRecord(ev[6], c->st));
     KM_CUDA(cudaStreamSynchronize(c->st));
     HostStat *h = c->hstat;
+    if (c->world <= 1) memcpy(h->global, h->local, sizeof h->global);
     if (first) {
         rec.changed = c->n_global;
         rec.dists = c->n_global * (int64_t)c->k;
