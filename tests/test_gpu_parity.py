@@ -395,3 +395,19 @@ def test_kmeanspp_multirun_matches_oracle():
     assert np.array_equal(bg[1], bo[1])
     assert centroid_rel_err(bg[2], bo[2]).max() <= 1e-12
     assert abs(bg[3] - bo[3]) <= 1e-12 * bo[3]
+
+
+@pytest.mark.parametrize("d,k", [(3, 1), (5, 7), (33, 4)])
+def test_skmeans_and_seed_odd_shapes(d, k):
+    """sk-means and k-means++ seeding with padded row widths (d -> DP) and k = 1."""
+    from paper_1902_09527_b200 import seed_plusplus
+    rng = np.random.default_rng(d * 100 + k)
+    X = (rng.normal(size=(5000, d)) + rng.normal(size=(1, d)) * 3).astype(np.float32)
+    u = rng.random(max(k - 1, 0))
+    ch_o, C_o = oracle.seed_plusplus(X, k, u, 17)
+    ch_g, C_g = seed_plusplus(X, k, u, 17)
+    assert ch_g.tolist() == ch_o.tolist() and np.array_equal(C_g, C_o)
+    r = oracle.skmeans(X, C_o, 50, 0)
+    g = gpu_run(X, C_g, 50, "mti", spherical=True)
+    assert g["iterations"] == r.iterations and np.array_equal(g["a"], r.a)
+    assert centroid_rel_err(g["C"], r.C).max() <= 1e-12
