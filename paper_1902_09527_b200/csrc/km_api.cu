@@ -474,10 +474,10 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         KM_CUDA(cudaMemsetAsync(c->a[i], 0, (size_t)c->n_alloc * sizeof(int32_t), c->st));
         KM_CUDA(cudaMemsetAsync(c->u[i], 0, (size_t)c->n_alloc * sizeof(float), c->st));
     }
-    // prefix classes per cluster: up to 32 while k*Q fits the scatter's 48 KB of bucket cursors
-    // (k = 100: 32; k = 1000: 12 classes of equal population)
-    c->Q = std::max(1, std::min(32, 12288 / k));
-    if (const char *e = getenv("KM_Q")) c->Q = std::max(1, std::min(12288 / k, atoi(e)));   // A/B
+    // prefix classes per cluster: up to 32 while k*Q <= KM_NB_MAX bucket cursors (scatter smem)
+    // (k = 100 and k = 1000: 32 classes of equal population)
+    c->Q = std::max(1, std::min(32, KM_NB_MAX / k));
+    if (const char *e = getenv("KM_Q")) c->Q = std::max(1, std::min(KM_NB_MAX / k, atoi(e)));   // A/B
     const int NBmax = k * c->Q;
     c->ntiles = (int)((n + c->tile_rows - 1) / c->tile_rows);
     KM_TRY(dalloc(&c->keys, (size_t)n));

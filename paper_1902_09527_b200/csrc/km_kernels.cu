@@ -638,6 +638,17 @@ __global__ void __launch_bounds__(512) k_scatter(SortParams p)
 
 cudaError_t launch_sort_tail(const SortParams &p, cudaStream_t st, int *launches);
 
+template <int DP>
+static cudaError_t launch_scatter(const SortParams &p, size_t sh, cudaStream_t st)
+{
+    if (sh > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_scatter<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+        if (e != cudaSuccess) return e;
+    }
+    k_scatter<DP><<<p.ntiles, 512, sh, st>>>(p);
+    return cudaSuccess;
+}
+
 // Quantile prefix classes.  The walk's cost per warp is the largest prefix p in it, so rows are
 // bucketed by p in classes of equal population (not equal width): pass 1 computes p per row and
 // its histogram, one CTA turns the histogram into the class map, pass 2 forms the bucket keys.
@@ -771,17 +782,19 @@ cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches)
 
 cudaError_t launch_sort_tail(const SortParams &p, cudaStream_t st, int *launches)
 {
-    const size_t sh = (size_t)p.NB * sizeof(uint32_t);   // NB <= 12288 -> <= 48 KB
+    const size_t sh = (size_t)p.NB * sizeof(uint32_t);   // bucket cursors (NB <= KM_NB_MAX)
     k_scan_tiles<<<p.NB, 1024, 0, st>>>(p);
     k_scan_buckets<<<1, 1024, 0, st>>>(p);
+    cudaError_t e = cudaSuccess;
     switch (p.DP) {
-    case 4: k_scatter<4><<<p.ntiles, 512, sh, st>>>(p); break;
-    case 8: k_scatter<8><<<p.ntiles, 512, sh, st>>>(p); break;
-    case 16: k_scatter<16><<<p.ntiles, 512, sh, st>>>(p); break;
-    case 32: k_scatter<32><<<p.ntiles, 512, sh, st>>>(p); break;
-    case 64: k_scatter<64><<<p.ntiles, 512, sh, st>>>(p); break;
+    case 4: e = launch_scatter<4>(p, sh, st); break;
+    case 8: e = launch_scatter<8>(p, sh, st); break;
+    case 16: e = launch_scatter<16>(p, sh, st); break;
+    case 32: e = launch_scatter<32>(p, sh, st); break;
+    case 64: e = launch_scatter<64>(p, sh, st); break;
     default: return cudaErrorInvalidValue;
     }
+    if (e != cudaSuccess) return e;
     if (launches) *launches += 3;
     return cudaGetLastError();
 }

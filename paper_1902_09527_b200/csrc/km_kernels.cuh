@@ -12,6 +12,9 @@
 //   f, s   fp32[k]             drift (rounded up) and 1/2 nearest-centroid distance (rounded down)
 //   acc    k x (DP+1) fp64     per-cluster sums (DP slots, padded ones stay 0) and count
 #pragma once
+#ifndef KM_NB_MAX
+#define KM_NB_MAX 32768   // re-bucketing: at most this many (cluster, prefix class) buckets (C5: Q = 32)
+#endif
 #include <cuda_runtime.h>
 #include <stdint.h>
 
