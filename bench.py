@@ -122,34 +122,50 @@ def traffic_from_profile(cfg: str, prune: str, kernel: str):
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_oracle_rate(X, C0, n_full: int, k: int, sample_rows: int, iters: int, spherical: bool = False):
-    """The fp64 oracle (oracle/, as it stands) on the first ``sample_rows`` rows: iteration 1
-    brute force untimed, then ``iters`` timed MTI iterations (oracle_mti_pass + block sums +
-    update).  Returns (full-workload iterations/s extrapolated by rows, seconds, threads)."""
+def oracle_full_run(X, C0, k: int, warm: int, timed: int, spherical: bool = False):
+    """The fp64 oracle (oracle/, as it stands, all host cores) on the FULL data set: iteration 1
+    (brute force, no bounds) and warm-1 further MTI iterations untimed, then ``timed`` MTI
+    iterations timed one by one (oracle_mti_pass + block sums + update: the same S1-S4 as a GPU
+    step).  Returns (iterations/s over the timed window, seconds per timed iteration, threads)."""
     import numpy as np
     import oracle
-    Xs = np.ascontiguousarray(X[:sample_rows])
+    Xs = X
     if spherical:   # sk-means: the oracle's projection and re-normalised update
         Xs, C0 = oracle.normalize_rows(Xs), oracle.normalize_centroids(C0)
     renorm = (lambda Cm, cnt, Cold: oracle.renormalize(Cm, cnt, Cold)) if spherical else (lambda Cm, cnt, Cold: Cm)
     a, d1, _ = oracle.assign_brute(Xs, C0)
     u = np.sqrt(d1)
+    del d1
     sums, counts = oracle.cluster_sums(Xs, a, k)
     C, _ = oracle.update(sums, counts, C0)
     C = renorm(C, counts, C0)
     Cprev = C0
-    t0 = time.perf_counter()
-    for _ in range(iters):
+    per = []
+    for i in range(max(0, warm - 1) + timed):
+        t0 = time.perf_counter()
         a, u, _, _, _ = oracle.mti_pass(Xs, C, Cprev, a, u)
         sums, counts = oracle.cluster_sums(Xs, a, k)
         Cprev, (C, _) = C, oracle.update(sums, counts, C)
         C = renorm(C, counts, Cprev)
-    dt = time.perf_counter() - t0
-    rate = iters / dt * (sample_rows / n_full)
-    return rate, dt, oracle.num_threads()
+        if i >= max(0, warm - 1):
+            per.append(time.perf_counter() - t0)
+    return len(per) / sum(per), per, oracle.num_threads()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, rank, world):
+    """Reference arm: the oracle (fp64, OpenMP on all host cores) runs the SAME workload as our
+    arm — the full data set of the config, iteration 1 + W-1 warm-up iterations untimed, then K
+    timed iterations (the same window as the GPU arm's timed iterations W+1..W+K)."""
     import numpy as np
     from synth import CONFIGS, make_config
     if rank != 0:
@@ -157,24 +173,22 @@ def run_reference(args, rank, world):
     spec = CONFIGS[args.config]
     X, idx, _ = make_config(args.config)
     C0 = X[idx].astype(np.float64)
-    sample = min(spec.n, 2_000_000 if spec.d <= 16 else 1_000_000)
-    if spec.k >= 1000:
-        sample = min(spec.n, 200_000)
-    # warm-up steps (untimed) then K timed oracle MTI iterations on the sample
     sph = args.algo == "skmeans"
-    cpu_oracle_rate(X, C0, spec.n, spec.k, sample, max(1, args.warmup), sph)
-    rate, dt, cores = cpu_oracle_rate(X, C0, spec.n, spec.k, sample, args.steps, sph)
+    rate, per, cores = oracle_full_run(X, C0, spec.k, max(1, args.warmup), args.steps, sph)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8(d) recipe, seed 0)",
-        "config": {"workload": f"{args.config}: n={spec.n}, d={spec.d}, k={spec.k}", "algo": args.algo, "prune": "mti",
-                   "parallelism": "host cores (OpenMP)"},
+        "config": {"workload": f"{args.config}: n={spec.n}, d={spec.d}, k={spec.k}, Forgy init, iterations "
+                               f"{max(1, args.warmup) + 1}..{max(1, args.warmup) + args.steps}",
+                   "algo": args.algo, "prune": "mti", "parallelism": "host cores (OpenMP)"},
         "effective_dists_per_s": rate * spec.n * spec.k,
+        "timed_s": sum(per),
         "cpu_baseline": {"value": rate, "unit": "iters/s", "cores": cores, "kind": "oracle",
-                         "sample": f"first {sample} rows of {args.config}, {args.steps} MTI iterations "
-                                   f"after 1 brute + {args.warmup} warm-up, extrapolated x{spec.n / sample:.2f} by rows"},
+                         "cpu": cpu_model(),
+                         "sample": f"full {args.config} (n={spec.n}), {args.steps} timed MTI iterations after "
+                                   f"iteration 1 (brute force) + {max(0, args.warmup - 1)} warm-up; no extrapolation"},
         "e2e": {"value": rate, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -215,7 +229,13 @@ def run_ours(args, rank, world, local_rank):
                 X[idx[own] - lo].astype(np.float64)).cuda()
         dist.all_reduce(rows)
         C0 = rows.cpu().numpy()
-        nccl_id = broadcast_bytes(nccl_unique_id() if rank == 0 else b"\0" * 128)
+
+    def fresh_nccl_id():
+        """A new ncclUniqueId for every communicator (an id serves one ncclCommInitRank)."""
+        if world == 1:
+            return None
+        return broadcast_bytes(nccl_unique_id() if rank == 0 else b"\0" * 128)
+    nccl_id = fresh_nccl_id()
 
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
     stream = torch.cuda.current_stream()
@@ -245,7 +265,8 @@ def run_ours(args, rank, world, local_rank):
     timed = stats[args.warmup:args.warmup + args.steps]
     assign_ms = [s["ms_assign"] for s in timed]
     avg_assign = sum(assign_ms) / len(assign_ms)
-    bytes_per_row = 4 * d + 16 if args.prune == "mti" else 4 * d + 16
+    # algorithmic bytes per row: MTI x + u r/w + a r/w; knori- x + a r/w
+    bytes_per_row = 4 * d + 16 if args.prune == "mti" else 4 * d + 8
     algo_bytes = (hi - lo) * bytes_per_row
     peak, peak_src = load_peaks()
     achieved = algo_bytes / (avg_assign * 1e-3) / 1e9
@@ -275,6 +296,13 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": engine,
                      "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": avg_assign,
                      "peak_source": peak_src},
+        # FP32 pipe: the centred expansion form spends ~d+2 FP32 lane-operations per
+        # computed distance; peak = 148 SMs x 128 lanes x sm clock (1.965 GHz max)
+        "fp32_pipe": {"model": "(d+2) FP32 lane-ops per computed distance (expansion form)",
+                      "achieved_ops_per_s": (d + 2) * (dists_computed / len(timed)) / (avg_assign * 1e-3),
+                      "peak_ops_per_s": 148 * 128 * 1.965e9,
+                      "frac": (d + 2) * (dists_computed / len(timed)) / (avg_assign * 1e-3) / (148 * 128 * 1.965e9)},
+        "hbm_frac_nominal_8tbs": achieved / 8000.0,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "final_sse": sse,
@@ -293,11 +321,12 @@ def run_ours(args, rank, world, local_rank):
         # DMA from a freshly pinned buffer pays a one-time mapping cost (measured: create 140 ms
         # instead of 45 ms for C3's 2.1 GB)
         for rep in range(2):
+            nid = fresh_nccl_id()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nccl_id, n_global=n,
+            km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nid, n_global=n,
                          spherical=args.algo == "skmeans",
                          device=local_rank)
             t1 = time.perf_counter()
@@ -322,14 +351,20 @@ def run_ours(args, rank, world, local_rank):
         del Xh
     # ---- CPU baseline: the oracle on the host cores (rank 0, N=1 only) ------------------------
     if world == 1 and not args.no_cpu_baseline:
-        sample = min(n, 2_000_000 if d <= 16 else 1_000_000)
-        if k >= 1000:
-            sample = min(n, 200_000)
-        it = 3
-        rate, dt, cores = cpu_oracle_rate(X, C0, n, k, sample, it, args.algo == "skmeans")
+        if n * k * d <= 65_608_366 * 100 * 8:
+            # the full data set (C3: iteration 1 brute force ~5 s + 2 MTI iterations on 16 cores)
+            rate, per, cores = oracle_full_run(X, C0, k, 1, 2, args.algo == "skmeans")
+            smp = (f"full {args.config} (n={n}), MTI iterations 2-3 timed after iteration 1 (brute force); "
+                   f"{sum(per):.1f} s timed; no extrapolation")
+        else:
+            # d = 32 / k = 1000: a prefix of the rows (a full brute-force iteration 1 of C5 takes minutes)
+            m = 2_000_000 if k <= 100 else 400_000
+            rate, per, cores = oracle_full_run(np.ascontiguousarray(X[:m]), C0, k, 1, 2, args.algo == "skmeans")
+            rate *= m / n
+            smp = (f"first {m} rows of {args.config}, MTI iterations 2-3 after iteration 1 ({sum(per):.1f} s), "
+                   f"scaled x{n / m:.1f} by rows (extrapolated: not the same workload)")
         line["cpu_baseline"] = {"value": rate, "unit": "iters/s", "cores": cores, "kind": "oracle",
-                                "sample": f"first {sample} rows of {args.config}, {it} MTI iterations "
-                                          f"after 1 brute ({dt:.1f} s), extrapolated x{n / sample:.2f} by rows"}
+                                "cpu": cpu_model(), "sample": smp}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -337,11 +372,29 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
+def relaunch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: start the N ranks ourselves (one process per
+    GPU, torch.distributed.run on 127.0.0.1) and return its exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local_rank)

@@ -141,6 +141,13 @@ km_status kmeans_run(km_ctx *ctx, int32_t max_iters, int64_t tol, int32_t *itera
  * out_is_device = 1 (device memory on the context device).  KM_ESTATE before iteration 1. */
 km_status kmeans_get_assignments(km_ctx *ctx, int32_t *out, int32_t out_is_device);
 
+/* Debug/verification: the n_local fp32 upper bounds u(x) kept by MTI after the last pass, in
+ * the caller's row order.  After a pass that used centroids C_used, u(x_i) >= ||x_i - C_used[a_i]||
+ * (exact real arithmetic on the fp64 C_used, bound loosened by drift and
+ * tightened by U(u)).  out is host memory unless out_is_device = 1.  KM_ESTATE before iteration
+ * 1 or with KM_PRUNE_NONE (no bounds are kept). */
+km_status kmeans_get_bounds(km_ctx *ctx, float *out, int32_t out_is_device);
+
 /* k x d fp64 current centroids C_T (host memory, caller-owned).  Identical on all ranks. */
 km_status kmeans_get_centroids(km_ctx *ctx, double *out_host);
 

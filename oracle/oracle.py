@@ -202,3 +202,50 @@ def lloyd(X, C0, max_iters, tol=0, mode="brute", shards=1, with_sse=True) -> Ora
     T = int(it[0])
     return OracleResult(a, C, T, ch[:T], ds[:T], c1[:T], em[:T],
                         ss[:T] if ss is not None else np.zeros(0))
+
+
+def lloyd_trace(X, C0, max_iters, tol=0, mode="mti", on_iter=None) -> OracleResult:
+    """The loop of ``oracle_lloyd`` (kmeans_oracle.c) driven step by step from Python over the
+    same C primitives, so that a caller can observe every iteration: ``on_iter(t, a_t, C_t,
+    record)`` is called after iteration t's update (a_t: this pass's assignments, C_t: the means
+    it produced; record: dict of changed/dists/clause1/empty/sse).  Same steps, same order:
+    iteration 1 brute force (u = exact distance), then brute force or one MTI pass
+    (geometry/drift of the centroids this pass uses, §3.3), block-ordered sums, update with
+    reading A10, SSE w.r.t. (C_t, a_t), stop iff changed <= tol (§4.1).  Pinned to
+    ``lloyd`` (bitwise) by tests/test_oracle_trace.py."""
+    X = _X(X)
+    n, d = X.shape
+    C = _C(C0, d).copy()
+    k = C.shape[0]
+    if n < 1 or k < 1 or k > n or max_iters < 0:
+        raise ValueError("lloyd_trace: usage error")
+    Cprev = C.copy()
+    a = np.zeros(n, np.int32)
+    u = None
+    recs = []
+    t = 0
+    for t in range(1, max_iters + 1):
+        clause1 = 0
+        if t == 1 or mode == "brute":
+            aprev = a
+            a, d1, _ = assign_brute(X, C)
+            dists = n * k
+            changed = n if t == 1 else int(np.count_nonzero(a != aprev))
+            if mode == "mti":
+                u = np.sqrt(d1)
+        else:
+            a, u, dists, clause1, changed = mti_pass(X, C, Cprev, a, u)
+        sums, counts = cluster_sums(X, a, k)
+        Cprev = C
+        C, empty = update(sums, counts, Cprev)
+        rec = dict(t=t, changed=int(changed), dists=int(dists), clause1=int(clause1),
+                   empty=int(empty), sse=sse(X, a, C))
+        recs.append(rec)
+        if on_iter is not None:
+            on_iter(t, a, C, rec)
+        if changed <= tol:
+            break
+    T = len(recs)
+    col = lambda key, dt: np.array([r[key] for r in recs], dt)  # noqa: E731
+    return OracleResult(a, C, T, col("changed", np.int64), col("dists", np.int64),
+                        col("clause1", np.int64), col("empty", np.int32), col("sse", np.float64))

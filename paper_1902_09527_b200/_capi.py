@@ -47,6 +47,7 @@ SIGNATURES = {
     "kmeans_run": (ct.c_int32, [ct.c_void_p, ct.c_int32, ct.c_int64, ct.POINTER(ct.c_int32),
                                 ct.POINTER(ct.c_int64)]),
     "kmeans_get_assignments": (ct.c_int32, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
+    "kmeans_get_bounds": (ct.c_int32, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
     "kmeans_get_centroids": (ct.c_int32, [ct.c_void_p, ct.c_void_p]),
     "kmeans_set_centroids": (ct.c_int32, [ct.c_void_p, ct.c_void_p]),
     "kmeans_sse": (ct.c_int32, [ct.c_void_p, ct.POINTER(ct.c_double)]),

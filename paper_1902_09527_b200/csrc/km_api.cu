@@ -726,6 +726,24 @@ km_status kmeans_get_assignments(km_ctx *c, int32_t *out, int32_t out_is_device)
     return KM_OK;
 }
 
+km_status kmeans_get_bounds(km_ctx *c, float *out, int32_t out_is_device)
+{
+    g_err.clear();
+    if (!c || !out) return fail(KM_EARG, "NULL argument");
+    if (c->t == 0) return fail(KM_ESTATE, "no assignment pass has run yet");
+    if (c->prune != KM_PRUNE_MTI) return fail(KM_ESTATE, "no bounds are kept with KM_PRUNE_NONE");
+    KM_CUDA(cudaSetDevice(c->device));
+    if (!c->a_out) KM_TRY(dalloc(&c->a_out, (size_t)c->n));
+    // u is 4-byte data in the context's row order: the int32 unpermute moves its bits
+    KM_CUDA(km::launch_unpermute(reinterpret_cast<const int32_t *>(c->u[c->cur]), c->perm[c->cur], c->n, c->a_out,
+                                 c->st));
+    c->launches += 1;
+    KM_CUDA(cudaMemcpyAsync(out, c->a_out, (size_t)c->n * sizeof(float),
+                            out_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    return KM_OK;
+}
+
 km_status kmeans_get_centroids(km_ctx *c, double *out)
 {
     g_err.clear();

@@ -184,7 +184,8 @@ k_assign(AssignParams p)
             }
             if (valid) {
                 p.a[row] = anew;
-                p.u[row] = unew;
+                // knori- (no pruning after iteration 1) keeps no bound: a read + write only
+                if (MODE != MODE_DENSE_REDUCE) p.u[row] = unew;
                 if (p.count_changed) c_changed += (anew != aold);
             }
         }

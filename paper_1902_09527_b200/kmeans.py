@@ -112,6 +112,12 @@ class KMeans:
         C.check(C.lib().kmeans_get_assignments(self._h, ct.c_void_p(a.ctypes.data), 0))
         return a
 
+    def bounds(self) -> np.ndarray:
+        """fp32[n_local] MTI upper bounds u(x) after the last pass (caller order; verification)."""
+        u = np.empty(self.n, np.float32)
+        C.check(C.lib().kmeans_get_bounds(self._h, ct.c_void_p(u.ctypes.data), 0))
+        return u
+
     def centroids(self) -> np.ndarray:
         c = np.empty((self.k, self.d), np.float64)
         C.check(C.lib().kmeans_get_centroids(self._h, ct.c_void_p(c.ctypes.data)))

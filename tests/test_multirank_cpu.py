@@ -82,3 +82,25 @@ def test_shard_bounds_cover():
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(G - 1))
             assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
+
+
+def test_bench_launcher_starts_n_ranks():
+    """`bench.py --gpus 2` without a torchrun environment starts 2 ranks itself
+    (torch.distributed.run on 127.0.0.1); on the reference arm rank 0 alone prints one JSON line
+    with n_gpus = 2 and rank 1 exits 0 without work.  A WORLD_SIZE that contradicts --gpus fails."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--config", "c1", "--steps", "2", "--warmup", "1"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    j = json.loads(lines[0])
+    assert j["impl"] == "reference" and j["n_gpus"] == 2 and j["steps"] == 2
+    bad = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2"],
+                         capture_output=True, text=True, env=dict(env, WORLD_SIZE="1"), timeout=120)
+    assert bad.returncode != 0
