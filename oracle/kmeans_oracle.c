@@ -18,6 +18,8 @@
  *   Lloyd's / objective Eq. 1 ..... §4.1, PAPER.md:1104-1130 (SSE reading, A15)
  *   ||Lloyd's merged MM step ...... §3.2, PAPER.md:1000-1011 (per-thread state + reduction)
  *   MTI clauses 1-3 ............... §3.3, PAPER.md:1013-1053 (with Elkan's 1/2, A1-A7)
+ *   Elkan TI baseline ............. §2, PAPER.md:876-885 ("triangle inequality (TI) with bounds",
+ *                                   O(kn) lower-bound matrix); SPEC.md:265-273 (reading B10)
  * Parity pins: every function is pinned by tests/test_oracle_*.py (hand-checked vectors,
  * closed forms, brute-force optima, scikit-learn).  "dists" (the distance-computation
  * count) is pinned only by the hand-checked B2 trace and 0 <= dists <= n*k: the paper's
@@ -275,7 +277,90 @@ void oracle_mti_pass(const float *X, int64_t n, int d, const double *C, int k,
 }
 
 /*
- * Full Lloyd's run (§4.1) from C0, brute force (mode 0) or MTI (mode 1).
+ * Lower bounds for Elkan's TI after a brute-force pass (iteration 1 computes every distance):
+ * L[i*k + c] = ||x_i - C[c]|| (fp64, sqrt of the direct-form squared distance).
+ */
+void oracle_all_dists(const float *X, int64_t n, int d, const double *C, int k, double *L)
+{
+    int64_t i;
+#pragma omp parallel for schedule(static)
+    for (i = 0; i < n; ++i)
+        for (int c = 0; c < k; ++c)
+            L[i * (int64_t)k + c] = sqrt(sqdist(X + i * (int64_t)d, C + (int64_t)c * d, d));
+}
+
+/*
+ * One pass of Elkan's TI, t >= 2 (the paper's pruning baseline: "triangle inequality (TI) with
+ * bounds", a lower-bound matrix of size O(kn); reading B10).
+ * Per point, with a0 = a[i]:
+ *   l[c] <- max(0, l[c] - f(c)) for every c; u <- u + f(a0)        (bounds loosened by drift)
+ *   if u <= s(a0): keep a0, 0 distances                             (Elkan step 2 = MTI clause 1)
+ *   else best = a0; for c = 0..k-1 in index order, c != best:
+ *     if u > l[c] and u > H[best][c]:                               (Elkan step 3 (i), (ii))
+ *       if not yet tightened: u <- d(x, C[a0]); l[a0] <- u; 1 distance  (step 3a, once per pass)
+ *       if u > l[c] and u > H[best][c]:                             (step 3b, tightened u)
+ *         q <- d(x, C[c])^2; l[c] <- sqrt(q); 1 distance
+ *         if q < q_best, or q == q_best and c < best: best <- c, u <- sqrt(q)   (running best)
+ *   a <- best.  Comparisons of candidates use squared distances (as brute force), bounds use
+ *   distances.  L is n x k row-major; a, u, L are updated in place.  out3 = {dists, clause1, changed}.
+ */
+void oracle_ti_pass(const float *X, int64_t n, int d, const double *C, int k,
+                    const double *H, const double *s, const double *f,
+                    int32_t *a, double *u, double *L, int64_t *out3)
+{
+    int64_t dists = 0, clause1 = 0, changed = 0, i;
+#pragma omp parallel for schedule(static) reduction(+ : dists, clause1, changed)
+    for (i = 0; i < n; ++i) {
+        const float *x = X + i * (int64_t)d;
+        double *l = L + i * (int64_t)k;
+        for (int c = 0; c < k; ++c) {
+            double v = l[c] - f[c];
+            l[c] = v > 0.0 ? v : 0.0;
+        }
+        const int32_t a0 = a[i];
+        double ui = u[i] + f[a0];
+        if (ui <= s[a0]) {                       /* clause 1 */
+            u[i] = ui;
+            clause1 += 1;
+            continue;
+        }
+        int32_t best = a0;
+        double bestq = INFINITY;
+        int tight = 0;
+        int64_t nd = 0;
+        for (int c = 0; c < k; ++c) {
+            if (c == best) continue;
+            const double h = H[(int64_t)best * k + c];
+            if (!(ui > l[c] && ui > h)) continue;
+            if (!tight) {                        /* step 3a: tighten u once */
+                bestq = sqdist(x, C + (int64_t)a0 * d, d);
+                ui = sqrt(bestq);
+                l[a0] = ui;
+                tight = 1;
+                nd += 1;
+                if (!(ui > l[c] && ui > h)) continue;
+            }
+            double q = sqdist(x, C + (int64_t)c * d, d);
+            nd += 1;
+            l[c] = sqrt(q);
+            if (q < bestq || (q == bestq && c < best)) {
+                bestq = q;
+                best = c;
+                ui = sqrt(q);
+            }
+        }
+        dists += nd;
+        if (best != a0) changed += 1;
+        a[i] = best;
+        u[i] = ui;
+    }
+    out3[0] = dists;
+    out3[1] = clause1;
+    out3[2] = changed;
+}
+
+/*
+ * Full Lloyd's run (§4.1) from C0, brute force (mode 0), MTI (mode 1) or Elkan TI (mode 2).
  *   iteration 1: brute-force assignment (no bounds exist), changed = n, dists = n*k,
  *                u = exact distance to the assigned centroid;
  *   iteration t >= 2: brute force (dists = n*k) or one MTI pass;
@@ -295,11 +380,15 @@ int oracle_lloyd(const float *X, int64_t n, int d, int k, const double *C0, int 
     double *Cprev = (double *)malloc(sizeof(double) * kd);
     double *sums = (double *)malloc(sizeof(double) * kd);
     int64_t *counts = (int64_t *)malloc(sizeof(int64_t) * k);
-    double *H = NULL, *s = NULL, *f = NULL, *u = NULL, *d1 = NULL;
+    double *H = NULL, *s = NULL, *f = NULL, *u = NULL, *d1 = NULL, *L = NULL;
     int32_t *aprev = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     memcpy(C, C0, sizeof(double) * kd);
     memcpy(Cprev, C0, sizeof(double) * kd);
-    if (mode == 1) {
+    if (mode == 2) {
+        L = (double *)malloc(sizeof(double) * (size_t)n * k);
+        if (!L) { free(Cprev); free(sums); free(counts); free(aprev); return -2; }
+    }
+    if (mode == 1 || mode == 2) {
         H = (double *)malloc(sizeof(double) * (size_t)k * k);
         s = (double *)malloc(sizeof(double) * k);
         f = (double *)malloc(sizeof(double) * k);
@@ -319,13 +408,15 @@ int oracle_lloyd(const float *X, int64_t n, int d, int k, const double *C0, int 
                 changed = 0;
                 for (int64_t i = 0; i < n; ++i) changed += (a[i] != aprev[i]);
             }
-            if (mode == 1)
+            if (mode >= 1)
                 for (int64_t i = 0; i < n; ++i) u[i] = sqrt(d1[i]);
+            if (mode == 2) oracle_all_dists(X, n, d, C, k, L);
         } else {
             int64_t o3[3];
             oracle_geometry(C, k, d, H, s);
             oracle_drift(C, Cprev, k, d, f);
-            oracle_mti_pass(X, n, d, C, k, H, s, f, a, u, o3);
+            if (mode == 1) oracle_mti_pass(X, n, d, C, k, H, s, f, a, u, o3);
+            else oracle_ti_pass(X, n, d, C, k, H, s, f, a, u, L, o3);
             dists = o3[0];
             c1 = o3[1];
             changed = o3[2];
@@ -344,6 +435,6 @@ int oracle_lloyd(const float *X, int64_t n, int d, int k, const double *C0, int 
     if (t > max_iters) t = max_iters;
     *iterations = t;
     free(Cprev); free(sums); free(counts); free(aprev);
-    free(H); free(s); free(f); free(u); free(d1);
+    free(H); free(s); free(f); free(u); free(d1); free(L);
     return 0;
 }

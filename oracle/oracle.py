@@ -47,6 +47,8 @@ def lib():
         L.oracle_lloyd.argtypes = [P, i64, ct.c_int, ct.c_int, P, ct.c_int, i64, ct.c_int,
                                    ct.c_int, P, P, P, P, P, P, P, P]
         L.oracle_lloyd.restype = ct.c_int
+        L.oracle_all_dists.argtypes = [P, i64, ct.c_int, P, ct.c_int, P]
+        L.oracle_ti_pass.argtypes = [P, i64, ct.c_int, P, ct.c_int, P, P, P, P, P, P, P]
         L.oracle_num_threads.restype = ct.c_int
         L.oracle_set_threads.argtypes = [ct.c_int]
         _lib = L
@@ -159,6 +161,33 @@ def mti_pass(X, C, Cprev, a, u):
     return a2, u2, int(o3[0]), int(o3[1]), int(o3[2])
 
 
+def all_dists(X, C):
+    """n x k fp64 matrix of ||x_i - C[c]|| (Elkan's lower bounds after iteration 1)."""
+    X = _X(X)
+    n, d = X.shape
+    C = _C(C, d)
+    L = np.empty((n, C.shape[0]), np.float64)
+    lib().oracle_all_dists(_p(X), n, d, _p(C), C.shape[0], _p(L))
+    return L
+
+
+def ti_pass(X, C, Cprev, a, u, L):
+    """One Elkan TI pass (t >= 2; kmeans_oracle.c oracle_ti_pass) with centroids C (previous pass
+    used Cprev): returns (a_new, u_new, L_new, dists, clause1, changed).  Inputs are not modified."""
+    X = _X(X)
+    n, d = X.shape
+    C, Cprev = _C(C, d), _C(Cprev, d)
+    k = C.shape[0]
+    H, s = geometry(C)
+    f = drift(C, Cprev)
+    a2 = np.array(a, dtype=np.int32, copy=True)
+    u2 = np.array(u, dtype=np.float64, copy=True)
+    L2 = np.array(L, dtype=np.float64, copy=True).reshape(n, k)
+    o3 = np.zeros(3, np.int64)
+    lib().oracle_ti_pass(_p(X), n, d, _p(C), k, _p(H), _p(s), _p(f), _p(a2), _p(u2), _p(L2), _p(o3))
+    return a2, u2, L2, int(o3[0]), int(o3[1]), int(o3[2])
+
+
 @dataclass
 class OracleResult:
     a: np.ndarray
@@ -185,7 +214,7 @@ def lloyd(X, C0, max_iters, tol=0, mode="brute", shards=1, with_sse=True) -> Ora
     n, d = X.shape
     C0 = _C(C0, d)
     k = C0.shape[0]
-    m = {"brute": 0, "mti": 1}[mode]
+    m = {"brute": 0, "mti": 1, "ti": 2}[mode]
     a = np.zeros(n, np.int32)
     C = np.empty((k, d), np.float64)
     it = np.zeros(1, np.int32)
@@ -197,6 +226,8 @@ def lloyd(X, C0, max_iters, tol=0, mode="brute", shards=1, with_sse=True) -> Ora
     ss = np.zeros(cap, np.float64) if with_sse else None
     rc = lib().oracle_lloyd(_p(X), n, d, k, _p(C0), int(max_iters), int(tol), m, int(shards),
                             _p(a), _p(C), _p(it), _p(ch), _p(ds), _p(c1), _p(em), _p(ss))
+    if rc == -2:
+        raise MemoryError("oracle_lloyd: TI lower-bound matrix (n x k fp64) could not be allocated")
     if rc != 0:
         raise ValueError("oracle_lloyd: usage error (n<1, d<1, k<1, k>n or max_iters<0)")
     T = int(it[0])
@@ -209,7 +240,8 @@ def lloyd_trace(X, C0, max_iters, tol=0, mode="mti", on_iter=None) -> OracleResu
     same C primitives, so that a caller can observe every iteration: ``on_iter(t, a_t, C_t,
     record)`` is called after iteration t's update (a_t: this pass's assignments, C_t: the means
     it produced; record: dict of changed/dists/clause1/empty/sse).  Same steps, same order:
-    iteration 1 brute force (u = exact distance), then brute force or one MTI pass
+    iteration 1 brute force (u = exact distance; TI: every distance as lower bounds), then
+    brute force, one MTI pass or one Elkan TI pass
     (geometry/drift of the centroids this pass uses, §3.3), block-ordered sums, update with
     reading A10, SSE w.r.t. (C_t, a_t), stop iff changed <= tol (§4.1).  Pinned to
     ``lloyd`` (bitwise) by tests/test_oracle_trace.py."""
@@ -221,7 +253,7 @@ def lloyd_trace(X, C0, max_iters, tol=0, mode="mti", on_iter=None) -> OracleResu
         raise ValueError("lloyd_trace: usage error")
     Cprev = C.copy()
     a = np.zeros(n, np.int32)
-    u = None
+    u = L = None
     recs = []
     t = 0
     for t in range(1, max_iters + 1):
@@ -231,8 +263,12 @@ def lloyd_trace(X, C0, max_iters, tol=0, mode="mti", on_iter=None) -> OracleResu
             a, d1, _ = assign_brute(X, C)
             dists = n * k
             changed = n if t == 1 else int(np.count_nonzero(a != aprev))
-            if mode == "mti":
+            if mode in ("mti", "ti"):
                 u = np.sqrt(d1)
+            if mode == "ti":
+                L = all_dists(X, C)
+        elif mode == "ti":
+            a, u, L, dists, clause1, changed = ti_pass(X, C, Cprev, a, u, L)
         else:
             a, u, dists, clause1, changed = mti_pass(X, C, Cprev, a, u)
         sums, counts = cluster_sums(X, a, k)

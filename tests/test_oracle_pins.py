@@ -52,7 +52,7 @@ def test_drift_inflate_example():
 
 
 # ---- hand-checked traces --------------------------------------------
-@pytest.mark.parametrize("mode", ["brute", "mti"])
+@pytest.mark.parametrize("mode", ["brute", "mti", "ti"])
 def test_B1_one_dim(mode):
     e = HV["B1"]
     r = oracle.lloyd(np.array(e["X"], np.float32), np.array(e["C0"], float), 100, 0, mode)
@@ -86,6 +86,27 @@ def test_B2_mti_trace():
     assert np.allclose(np.sqrt(d1), e["u_1"], atol=1e-12)
 
 
+def test_B2_ti_trace():
+    """Elkan TI (reading B10) on the B2 data: the hand-checked trace and the per-point state
+    (assignments, upper bounds, n x k lower bounds) after iteration 2."""
+    e, e2 = HV["B2"], HV["B2_TI"]
+    X = np.array(e["X"], np.float32)
+    C0 = X[e["forgy"]].astype(float)
+    r = oracle.lloyd(X, C0, 100, 0, "ti")
+    assert r.iterations == e2["iterations"] and r.dists.tolist() == e2["dists"]
+    assert r.changed.tolist() == e2["changed"] and r.clause1.tolist() == e2["clause1"]
+    assert np.allclose(r.C, np.array(e["C_T"], float), rtol=0, atol=1e-12)
+    assert abs(r.final_sse - e["sse"]) < 1e-9 and r.dists_total == e2["dists_total"]
+    a1, d1, _ = oracle.assign_brute(X, C0)
+    L1 = oracle.all_dists(X, C0)
+    assert np.allclose(L1, np.abs(X.astype(float) - C0.ravel()[None, :]), atol=1e-12)
+    C1 = np.array(e["C_1"], float)
+    a2, u2, L2, dists, c1, ch = oracle.ti_pass(X, C1, C0, a1, np.sqrt(d1), L1)
+    st = e2["state_2"]
+    assert a2.tolist() == st["a"] and (dists, c1, ch) == (st["dists"], st["clause1"], st["changed"])
+    assert np.allclose(u2, st["u"], atol=1e-12) and np.allclose(L2, np.array(st["L"], float), atol=1e-12)
+
+
 def test_B3_half_factor():
     """The literal clause (no 1/2) would keep x in a; with Elkan's 1/2 it moves (A1)."""
     e = HV["B3"]
@@ -97,7 +118,7 @@ def test_B3_half_factor():
     assert e["u"] <= np.linalg.norm(C[0] - C[1])
 
 
-@pytest.mark.parametrize("mode", ["brute", "mti"])
+@pytest.mark.parametrize("mode", ["brute", "mti", "ti"])
 def test_B5_empty_cluster(mode):
     e = HV["B5"]
     X = np.array(e["X"], np.float32)
@@ -126,18 +147,18 @@ def test_usage_errors():
 
 
 # ---- closed forms / special cases ----------------------------------------------------------
-@pytest.mark.parametrize("mode", ["brute", "mti"])
+@pytest.mark.parametrize("mode", ["brute", "mti", "ti"])
 def test_k1_global_mean(mode):
     rng = np.random.default_rng(5)
     X = rng.normal(size=(257, 3)).astype(np.float32)
     r = oracle.lloyd(X, X[:1].astype(float), 10, 0, mode)
     mean = np.array([math.fsum(float(v) for v in X[:, j]) / 257 for j in range(3)])
     assert r.iterations == 2 and np.allclose(r.C[0], mean, rtol=0, atol=1e-14)
-    if mode == "mti":   # s = +inf: every point is clause-1 from iteration 2
+    if mode != "brute":   # s = +inf: every point is clause-1 from iteration 2
         assert r.dists.tolist() == [257, 0] and r.clause1.tolist() == [0, 257]
 
 
-@pytest.mark.parametrize("mode", ["brute", "mti"])
+@pytest.mark.parametrize("mode", ["brute", "mti", "ti"])
 def test_k_equals_n(mode):
     X = np.array([[0, 0], [1, 0], [0, 3], [7, 7], [2, 9]], np.float32)
     r = oracle.lloyd(X, X.astype(float), 10, 0, mode)
@@ -214,14 +235,14 @@ def test_enumerator_matches_1d_dp(seed):
 def test_lloyd_vs_global_optimum(seed, n, k, d):
     X = np.random.default_rng(seed).normal(size=(n, d)).astype(np.float32)
     opt, lab = _opt_enum(X, k)
-    for mode in ("brute", "mti"):
+    for mode in ("brute", "mti", "ti"):
         for idx in itertools.combinations(range(n), k):
             r = oracle.lloyd(X, X[list(idx)].astype(float), 100, 0, mode)
             assert r.final_sse >= opt - 1e-9
     # Lloyd from the optimal partition's centroids is a fixed point with SSE_opt
     lab = np.asarray(lab)
     Copt = np.stack([X[lab == c].astype(float).mean(axis=0) for c in range(k)])
-    for mode in ("brute", "mti"):
+    for mode in ("brute", "mti", "ti"):
         r = oracle.lloyd(X, Copt, 100, 0, mode)
         assert r.changed[-1] == 0 and r.iterations == 2
         assert abs(r.final_sse - opt) <= 1e-12 * max(1.0, opt)
@@ -265,6 +286,38 @@ def test_mti_lossless_and_monotone(seed, n, d, k):
         sums, counts = oracle.cluster_sums(X, am, k)
         C_prev, (C, _) = C, oracle.update(sums, counts, C)
         a, u = am, um
+
+
+@pytest.mark.parametrize("seed,n,d,k", [(0, 3000, 4, 8), (1, 5000, 8, 20), (2, 2000, 3, 50), (3, 4000, 16, 12)])
+def test_ti_lossless_sound_and_fewer_dists_than_mti(seed, n, d, k):
+    """Elkan TI (reading B10): identical assignments/centroids to brute force at every
+    iteration, sound bounds after every pass (u >= d(x, C[a]), l[c] <= d(x, C[c]) for every c),
+    and never more distances than MTI in the same iteration (TI's extra bounds only
+    remove computations)."""
+    X = _mixture(seed, n, d, max(2, k // 2))
+    idx = np.random.default_rng(seed + 100).choice(n, k, replace=False)
+    C0 = X[idx].astype(float)
+    rb = oracle.lloyd(X, C0, 60, 0, "brute")
+    rm = oracle.lloyd(X, C0, 60, 0, "mti")
+    rt = oracle.lloyd(X, C0, 60, 0, "ti")
+    assert rt.iterations == rb.iterations
+    assert np.array_equal(rt.a, rb.a) and np.array_equal(rt.C, rb.C) and np.array_equal(rt.changed, rb.changed)
+    assert rt.dists[0] == n * k and np.all(rt.dists <= rm.dists) and np.all(rt.dists >= 0)
+    a, d1, _ = oracle.assign_brute(X, C0)
+    u, L = np.sqrt(d1), oracle.all_dists(X, C0)
+    sums, counts = oracle.cluster_sums(X, a, k)
+    C_prev, (C, _) = C0, oracle.update(sums, counts, C0)
+    Xd = X.astype(float)
+    for t in range(2, 8):
+        at, ut, Lt, dists, c1, ch = oracle.ti_pass(X, C, C_prev, a, u, L)
+        ab, _, _ = oracle.assign_brute(X, C)
+        assert np.array_equal(at, ab)
+        true = np.sqrt(((Xd[:, None, :] - C[None, :, :]) ** 2).sum(axis=2))
+        assert np.all(Lt <= true * (1 + 1e-15))
+        assert np.all(ut >= true[np.arange(n), at] * (1 - 1e-15))
+        sums, counts = oracle.cluster_sums(X, at, k)
+        C_prev, (C, _) = C, oracle.update(sums, counts, C)
+        a, u, L = at, ut, Lt
 
 
 def test_sharded_equals_unsharded():
