@@ -35,7 +35,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=27)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
-    ap.add_argument("--prune", default="mti", choices=["mti", "none"])
+    ap.add_argument("--prune", default="mti", choices=["mti", "none", "ti"],
+                    help="mti: the paper's method; none: knori- (all k distances); ti: Elkan's TI baseline")
     ap.add_argument("--algo", default="kmeans", choices=["kmeans", "skmeans"],
                     help="skmeans: spherical k-means (PAPER.md §4.2) on the same engine")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -265,12 +266,14 @@ def run_ours(args, rank, world, local_rank):
     timed = stats[args.warmup:args.warmup + args.steps]
     assign_ms = [s["ms_assign"] for s in timed]
     avg_assign = sum(assign_ms) / len(assign_ms)
-    # algorithmic bytes per row: MTI x + u r/w + a r/w; knori- x + a r/w
-    bytes_per_row = 4 * d + 16 if args.prune == "mti" else 4 * d + 8
+    # algorithmic bytes per row: MTI x + u r/w + a r/w; knori- x + a r/w;
+    # TI additionally reads and writes its k fp32 lower bounds
+    bytes_per_row = {"mti": 4 * d + 16, "none": 4 * d + 8, "ti": 4 * d + 16 + 8 * k}[args.prune]
     algo_bytes = (hi - lo) * bytes_per_row
     peak, peak_src = load_peaks()
     achieved = algo_bytes / (avg_assign * 1e-3) / 1e9
     sse = km.sse()
+    dev_bytes = km.device_bytes
     km.close()
     del Xd
     torch.cuda.empty_cache()
@@ -303,6 +306,7 @@ def run_ours(args, rank, world, local_rank):
                       "peak_ops_per_s": 148 * 128 * 1.965e9,
                       "frac": (d + 2) * (dists_computed / len(timed)) / (avg_assign * 1e-3) / (148 * 128 * 1.965e9)},
         "hbm_frac_nominal_8tbs": achieved / 8000.0,
+        "device_bytes": dev_bytes,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "final_sse": sse,

@@ -47,7 +47,11 @@ enum {
     KM_ESTATE = 6       /* call not valid in the current state (e.g. sse before any iteration) */
 };
 
-enum { KM_PRUNE_MTI = 0, KM_PRUNE_NONE = 1 };
+/* MTI: the paper's Minimal Triangle Inequality (knori, §3.3).  NONE: every distance
+ * (knori-).  TI: Elkan's triangle inequality with an n x k lower-bound matrix, the baseline the
+ * paper compares MTI with (§2, 876-885; claims 17-24); needs k * n_local * 4 bytes of
+ * device memory for the bounds (KM_ENOMEM otherwise) and keeps the caller's row order. */
+enum { KM_PRUNE_MTI = 0, KM_PRUNE_NONE = 1, KM_PRUNE_TI = 2 };
 
 /* Row re-bucketing policy: the context keeps its own copy of
  * the points physically sorted by (assigned cluster, survivor-prefix class) so that warps
@@ -64,7 +68,8 @@ enum { KM_ENGINE_AUTO = 0, KM_ENGINE_CUDA_CORE = 1, KM_ENGINE_TENSOR = 2 };
 typedef struct km_options {
     int32_t device;            /* CUDA device ordinal the context lives on */
     void *stream;              /* cudaStream_t, borrowed; NULL = the context creates its own */
-    int32_t prune;             /* KM_PRUNE_MTI (knori) or KM_PRUNE_NONE (knori-, all k distances) */
+    int32_t prune;             /* KM_PRUNE_MTI (knori), KM_PRUNE_NONE (knori-, all k distances) or
+                                  KM_PRUNE_TI (Elkan baseline) */
     int32_t rank;              /* this process's rank, 0 <= rank < world */
     int32_t world;             /* number of ranks (GPUs); 1 = no collective */
     uint8_t nccl_unique_id[128]; /* ncclUniqueId from kmeans_nccl_unique_id() on rank 0 (world > 1) */
@@ -178,9 +183,12 @@ km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *poi
 /* Number of kernel launches this context has issued so far (for launch accounting). */
 int64_t kmeans_launch_count(const km_ctx *ctx);
 
+/* Bytes of device memory the context holds (points copy, per-row state, bounds, scratch). */
+int64_t kmeans_device_bytes(const km_ctx *ctx);
+
 /* Name of the kernel that runs the MTI assignment pass (S2+S3) of this context:
  * "k_walk" (CUDA-core walk engine), "k_mti_tc" (tcgen05 engine), "k_assign" (direct-form lane
- * walk, legacy) or "k_assign_dense" (KM_PRUNE_NONE).  Static string; NULL ctx -> "". */
+ * walk, legacy), "k_assign_dense" (KM_PRUNE_NONE) or "k_ti" (KM_PRUNE_TI).  Static string; NULL ctx -> "". */
 const char *kmeans_engine(const km_ctx *ctx);
 
 /* Release all device memory, the internal stream (if created) and the NCCL communicator. */

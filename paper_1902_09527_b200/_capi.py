@@ -14,7 +14,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("KM_LIB") or os.path.join(_PKG, "libkmeans_b200.so")
 
 KM_OK, KM_EARG, KM_ENONFINITE, KM_ECUDA, KM_ENCCL, KM_ENOMEM, KM_ESTATE = range(7)
-KM_PRUNE_MTI, KM_PRUNE_NONE = 0, 1
+KM_PRUNE_MTI, KM_PRUNE_NONE, KM_PRUNE_TI = 0, 1, 2
 KM_RESORT_AUTO, KM_RESORT_NEVER, KM_RESORT_ALWAYS = 0, 1, 2
 KM_ENGINE_AUTO, KM_ENGINE_CUDA_CORE, KM_ENGINE_TENSOR = 0, 1, 2
 STATUS_NAMES = {0: "KM_OK", 1: "KM_EARG", 2: "KM_ENONFINITE", 3: "KM_ECUDA", 4: "KM_ENCCL",
@@ -57,6 +57,7 @@ SIGNATURES = {
                                           ct.c_int64, ct.c_void_p, ct.c_int32, ct.c_void_p, ct.c_void_p,
                                           ct.c_void_p]),
     "kmeans_launch_count": (ct.c_int64, [ct.c_void_p]),
+    "kmeans_device_bytes": (ct.c_int64, [ct.c_void_p]),
     "kmeans_engine": (ct.c_char_p, [ct.c_void_p]),
     "kmeans_destroy": (None, [ct.c_void_p]),
     "kmeans_last_error": (ct.c_char_p, []),

@@ -27,6 +27,7 @@
 namespace {
 
 thread_local std::string g_err;
+thread_local size_t *g_track = nullptr;   // device bytes of the context being created
 
 km_status fail(km_status s, const char *fmt, ...)
 {
@@ -176,6 +177,11 @@ struct km_ctx {
     bool spherical = false;         // sk-means (rows and centroids on the unit sphere)
     int resort_policy = KM_RESORT_AUTO;
     float resort_fraction = 0.10f;
+    // Elkan TI baseline (KM_PRUNE_TI): k x n_alloc lower bounds (centroid-major), H in index order
+    bool use_ti = false;
+    float *L = nullptr, *Hm = nullptr;
+    int ti_grid = 0;
+    size_t dev_bytes = 0;           // device memory held by the context
     std::vector<km_iter_stats> stats;
     cudaEvent_t ev[7] = {};
     ncclComm_t comm = nullptr;
@@ -204,6 +210,10 @@ km_status prep(km_ctx *c)
     if (c->use_walk) {
         KM_CUDA(km::launch_prep_walk(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->wpad, c->whs, c->Wblk, c->Wcc, c->Wmeta, c->WH,
                                      c->st));
+        c->launches += 1;
+    }
+    if (c->use_ti) {
+        KM_CUDA(km::launch_prep_ti(c->NL, c->k, c->ks, c->Hm, c->st));
         c->launches += 1;
     }
     if (c->use_tc) {
@@ -258,7 +268,9 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
 km_status launch_assign(km_ctx *c, int mode, int work_slot)
 {
     km::AssignParams p = assign_params(c, work_slot);
-    if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
+    if (c->use_ti && (mode == km::MODE_MTI_REDUCE || mode == km::MODE_DENSE)) {
+        KM_CUDA(km::launch_ti(c->DP, c->csmem, mode == km::MODE_DENSE, p, c->L, c->n_alloc, c->Hm, c->ti_grid, c->st));
+    } else if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
         if (c->use_tc) KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
         else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->st));
         if (c->use_tc || !c->wh_smem) {   // deferred distance counts (misfit rows)
@@ -354,7 +366,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
     KM_TRY(prep(c));
     KM_CUDA(cudaEventRecord(ev[2], c->st));
-    c->delta_pass = !first && (c->use_walk || c->use_tc);
+    c->delta_pass = !first && (c->use_walk || c->use_tc || c->use_ti);
     if (first) {
         KM_TRY(launch_assign(c, km::MODE_DENSE, 0));
         KM_CUDA(cudaEventRecord(ev[3], c->st));
@@ -364,7 +376,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
         }
         KM_TRY(launch_assign(c, km::MODE_REDUCE_ONLY, 1));
     } else {
-        KM_TRY(launch_assign(c, c->prune == KM_PRUNE_MTI ? km::MODE_MTI_REDUCE : km::MODE_DENSE_REDUCE, 0));
+        KM_TRY(launch_assign(c, c->prune != KM_PRUNE_NONE ? km::MODE_MTI_REDUCE : km::MODE_DENSE_REDUCE, 0));
         KM_CUDA(cudaEventRecord(ev[3], c->st));
     }
     KM_CUDA(cudaEventRecord(ev[4], c->st));
@@ -420,7 +432,7 @@ void free_all(km_ctx *c)
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base); cudaFree(c->lohist); cudaFree(c->qmap);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
     cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
-    cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part);
+    cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part); cudaFree(c->L); cudaFree(c->Hm);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
     if (c->comm) { NcclApi *N = nccl(); if (N) N->CommDestroy(c->comm); }
@@ -431,8 +443,11 @@ template <typename T>
 km_status dalloc(T **p, size_t count)
 {
     cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), std::max<size_t>(count, 1) * sizeof(T));
-    if (e != cudaSuccess)
+    if (e != cudaSuccess) {
+        cudaGetLastError();   // not sticky: clear it so later launches do not report it
         return fail(KM_ENOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+    }
+    if (g_track) *g_track += std::max<size_t>(count, 1) * sizeof(T);
     return KM_OK;
 }
 
@@ -445,6 +460,8 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     c->prune = o->prune; c->rank = o->rank; c->world = o->world;
     c->n_global = o->n_global > 0 ? o->n_global : n * (int64_t)o->world;
     c->resort_policy = o->resort_policy;
+    c->use_ti = o->prune == KM_PRUNE_TI;
+    if (c->use_ti) c->resort_policy = KM_RESORT_NEVER;   // n x k bounds stay with the caller's rows
     c->resort_fraction = o->resort_fraction > 0.f ? o->resort_fraction : 0.10f;
     c->spherical = o->spherical != 0;
     KM_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
@@ -496,7 +513,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     KM_CUDA(cudaMemset(c->NL, 0, (size_t)(k + 1) * c->ks * sizeof(uint64_t)));
     const size_t acc_bytes = (size_t)k * (DP + 1) * sizeof(double);
     c->scratch_bytes = acc_bytes + 8 * sizeof(unsigned long long) + 8 * sizeof(int);
-    KM_CUDA(cudaMalloc(&c->scratch, c->scratch_bytes));
+    KM_TRY(dalloc(reinterpret_cast<char **>(&c->scratch), c->scratch_bytes));
     c->acc = static_cast<double *>(c->scratch);
     c->counters = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->scratch) + acc_bytes);
     int *ints = reinterpret_cast<int *>(c->counters + 8);
@@ -561,7 +578,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     }
     // AUTO: the CUDA-core walk (measured faster than the tensor-core pipeline on C3 and C4 so
     // far); KM_ENGINE_TENSOR selects the tcgen05 kernel
-    c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 &&
+    c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 && !c->use_ti &&
                 (o->engine == KM_ENGINE_TENSOR || (o->engine == KM_ENGINE_AUTO && getenv("KM_AUTO_TC")));
     if (o->engine == KM_ENGINE_TENSOR && !km::tc_supported(DP))
         return fail(KM_EARG, "tensor engine needs d padded to 8, 16 or 32 (d=%d)", d);
@@ -587,7 +604,17 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     }
     // CUDA-core engine: the centred expansion-form walk (k_walk); KM_LEGACY_WALK=1 keeps the
     // direct-form lane walk of k_assign for A/B comparison
-    c->use_walk = !c->use_tc && c->prune == KM_PRUNE_MTI && k >= 2 && km::walk_supported(DP) &&
+    if (c->use_ti) {
+        // Elkan's O(nk) lower-bound matrix: fp32, centroid-major
+        const size_t lbytes = (size_t)k * c->n_alloc * sizeof(float);
+        if (dalloc(&c->L, (size_t)k * c->n_alloc) != KM_OK)
+            return fail(KM_ENOMEM, "TI lower-bound matrix: k x n = %d x %lld fp32 = %.1f GB does not fit on the device",
+                        k, (long long)c->n_alloc, lbytes / 1e9);
+        KM_TRY(dalloc(&c->Hm, (size_t)k * k));
+        c->ti_grid = km::ti_grid(DP, c->csmem, k, c->num_sms);
+        c->part_grid = std::max(c->part_grid, c->ti_grid);
+    }
+    c->use_walk = !c->use_tc && !c->use_ti && c->prune == KM_PRUNE_MTI && k >= 2 && km::walk_supported(DP) &&
                   !getenv("KM_LEGACY_WALK");
     if (c->use_walk) {
         c->wpad = (k + 1) & ~1;                    // k-1 neighbours + >= 1 dummy row, even
@@ -668,11 +695,13 @@ km_status kmeans_create(int64_t n_local, int32_t d, int32_t k, const float *poin
     if (!points || !init_centroids) return fail(KM_EARG, "points/init_centroids is NULL");
     if (reinterpret_cast<uintptr_t>(points) % 4) return fail(KM_EARG, "points not 4-byte aligned");
     if (o.rank < 0 || o.rank >= o.world) return fail(KM_EARG, "rank=%d world=%d", o.rank, o.world);
-    if (o.prune != KM_PRUNE_MTI && o.prune != KM_PRUNE_NONE) return fail(KM_EARG, "prune=%d", o.prune);
+    if (o.prune != KM_PRUNE_MTI && o.prune != KM_PRUNE_NONE && o.prune != KM_PRUNE_TI) return fail(KM_EARG, "prune=%d", o.prune);
     if (o.resort_policy < 0 || o.resort_policy > 2) return fail(KM_EARG, "resort_policy=%d", o.resort_policy);
     o.n_global = ng;
     km_ctx *c = new km_ctx();
+    g_track = &c->dev_bytes;
     km_status s = create(n_local, d, k, points, init_centroids, &o, c);
+    g_track = nullptr;
     if (s != KM_OK) {
         std::string keep = g_err;
         free_all(c);
@@ -731,7 +760,7 @@ km_status kmeans_get_bounds(km_ctx *c, float *out, int32_t out_is_device)
     g_err.clear();
     if (!c || !out) return fail(KM_EARG, "NULL argument");
     if (c->t == 0) return fail(KM_ESTATE, "no assignment pass has run yet");
-    if (c->prune != KM_PRUNE_MTI) return fail(KM_ESTATE, "no bounds are kept with KM_PRUNE_NONE");
+    if (c->prune == KM_PRUNE_NONE) return fail(KM_ESTATE, "no bounds are kept with KM_PRUNE_NONE");
     KM_CUDA(cudaSetDevice(c->device));
     if (!c->a_out) KM_TRY(dalloc(&c->a_out, (size_t)c->n));
     // u is 4-byte data in the context's row order: the int32 unpermute moves its bits
@@ -798,10 +827,13 @@ km_status kmeans_get_stats(km_ctx *c, km_iter_stats *out, int32_t cap, int32_t *
 
 int64_t kmeans_launch_count(const km_ctx *c) { return c ? c->launches : 0; }
 
+int64_t kmeans_device_bytes(const km_ctx *c) { return c ? (int64_t)c->dev_bytes : 0; }
+
 const char *kmeans_engine(const km_ctx *c)
 {
     if (!c) return "";
-    if (c->prune != KM_PRUNE_MTI) return "k_assign_dense";
+    if (c->prune == KM_PRUNE_NONE) return "k_assign_dense";
+    if (c->use_ti) return "k_ti";
     return c->use_tc ? "k_mti_tc" : (c->use_walk ? "k_walk" : "k_assign");
 }
 

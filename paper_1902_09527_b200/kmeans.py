@@ -68,7 +68,7 @@ class KMeans:
         self._keep.append(C0)
         if stream is not None:
             o.stream = ct.c_void_p(int(stream))
-        o.prune = {"mti": C.KM_PRUNE_MTI, "none": C.KM_PRUNE_NONE}[prune]
+        o.prune = {"mti": C.KM_PRUNE_MTI, "none": C.KM_PRUNE_NONE, "ti": C.KM_PRUNE_TI}[prune]
         o.rank, o.world, o.n_global = rank, world, n_global
         if nccl_id is not None:
             o.nccl_unique_id[:] = list(nccl_id)
@@ -142,6 +142,11 @@ class KMeans:
     @property
     def launch_count(self) -> int:
         return int(C.lib().kmeans_launch_count(self._h))
+
+    @property
+    def device_bytes(self) -> int:
+        """Device memory held by the context (bytes)."""
+        return int(C.lib().kmeans_device_bytes(self._h))
 
     @property
     def engine(self) -> str:
