@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats-out", default=None)
+    ap.add_argument("--no-graph", action="store_true", help="launch each iteration eagerly (no CUDA graph)")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="run the NCCL allreduce even at N = 1 (1-rank communicator)")
     return ap.parse_args()
 
 
@@ -234,14 +237,14 @@ def run_ours(args, rank, world, local_rank):
     def fresh_nccl_id():
         """A new ncclUniqueId for every communicator (an id serves one ncclCommInitRank)."""
         if world == 1:
-            return None
+            return nccl_unique_id() if args.force_comm else None
         return broadcast_bytes(nccl_unique_id() if rank == 0 else b"\0" * 128)
     nccl_id = fresh_nccl_id()
 
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
     stream = torch.cuda.current_stream()
     km = KMeans(Xd, C0, prune=args.prune, stream=stream.cuda_stream, rank=rank, world=world,
-                spherical=args.algo == "skmeans",
+                spherical=args.algo == "skmeans", graph=not args.no_graph, force_comm=args.force_comm,
                 nccl_id=nccl_id, n_global=n)
     for _ in range(args.warmup):
         km.iterate()
@@ -290,6 +293,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": f"{args.config}: n={n}, d={d}, k={k}, Forgy init, iterations "
                                f"{args.warmup + 1}..{args.warmup + args.steps}",
                    "algo": args.algo, "prune": args.prune, "parallelism": f"rows sharded over {world} GPU(s)",
+                   "launch": "eager" if args.no_graph else "CUDA graph per iteration (t >= 2)",
+                   "collective": "NCCL allreduce" if (world > 1 or args.force_comm) else "none (1 GPU)",
                    "l2": f"inputs {n * 4 * d / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "effective_dists_per_s": iters_per_s * n * k,
         "dists_computed_per_s": dists_computed / (ms_max * 1e-3),
@@ -331,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nid, n_global=n,
-                         spherical=args.algo == "skmeans",
+                         spherical=args.algo == "skmeans", graph=not args.no_graph, force_comm=args.force_comm,
                          device=local_rank)
             t1 = time.perf_counter()
             for _ in range(total_iters):

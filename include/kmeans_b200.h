@@ -85,7 +85,13 @@ typedef struct km_options {
                                   likewise (fp64), and every update re-normalises the mean (fp64);
                                   assignment = Euclidean argmin on the sphere = cosine argmax, so MTI
                                   applies unchanged.  A zero row or zero initial centroid is KM_EARG. */
-    int32_t reserved[6];
+    int32_t no_graph;          /* 1 = launch every kernel of an iteration eagerly; 0 (default) = from
+                                  iteration 2 on, the iteration (S1-S4 + allreduce + counter read-back)
+                                  is captured once per row buffer as a CUDA graph and replayed */
+    int32_t force_comm;        /* 1 = create the NCCL communicator and run the allreduce even when
+                                  world == 1 (a 1-rank communicator; needs nccl_unique_id): exercises
+                                  the multi-GPU data path on one GPU */
+    int32_t reserved[4];
 } km_options;
 
 typedef struct km_iter_stats {

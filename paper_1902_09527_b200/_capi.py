@@ -27,7 +27,8 @@ class KmOptions(ct.Structure):
                 ("nccl_unique_id", ct.c_uint8 * 128), ("n_global", ct.c_int64),
                 ("check_finite", ct.c_int32), ("points_on_host", ct.c_int32),
                 ("resort_policy", ct.c_int32), ("resort_fraction", ct.c_float),
-                ("engine", ct.c_int32), ("spherical", ct.c_int32), ("reserved", ct.c_int32 * 6)]
+                ("engine", ct.c_int32), ("spherical", ct.c_int32), ("no_graph", ct.c_int32),
+                ("force_comm", ct.c_int32), ("reserved", ct.c_int32 * 4)]
 
 
 class KmIterStats(ct.Structure):

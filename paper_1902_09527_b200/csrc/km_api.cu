@@ -159,7 +159,6 @@ struct km_ctx {
     size_t scratch_bytes = 0;
     double *acc = nullptr;          // k x (DP+1) reduced sums | counts (allreduce buffer)
     double *S = nullptr;            // k x (DP+1) running sums | counts (delta passes add to it)
-    bool delta_pass = false;        // this iteration's pass reduced only the moves
     double *acc_part = nullptr;     // grid x k x (DP+1) per-CTA partials
     int part_grid = 0;
     int nslab = 0;                  // number of partial slabs (= SM count)
@@ -185,6 +184,11 @@ struct km_ctx {
     std::vector<km_iter_stats> stats;
     cudaEvent_t ev[7] = {};
     ncclComm_t comm = nullptr;
+    bool comm_on = false;           // allreduce runs (world > 1, or force_comm)
+    // CUDA graph of one iteration t >= 2 (S1-S4 + allreduce + counter copy), one per row buffer
+    bool use_graph = true;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int64_t glaunches[2] = {0, 0};  // kernels in each graph
     int64_t launches = 0;
 };
 
@@ -269,7 +273,7 @@ km_status launch_assign(km_ctx *c, int mode, int work_slot)
 {
     km::AssignParams p = assign_params(c, work_slot);
     if (c->use_ti && (mode == km::MODE_MTI_REDUCE || mode == km::MODE_DENSE)) {
-        KM_CUDA(km::launch_ti(c->DP, c->csmem, mode == km::MODE_DENSE, p, c->L, c->n_alloc, c->Hm, c->ti_grid, c->st));
+        KM_CUDA(km::launch_ti(c->DP, c->csmem, mode == km::MODE_DENSE, p, c->L, c->Hm, c->ti_grid, c->st));
     } else if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
         if (c->use_tc) KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
         else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->st));
@@ -298,7 +302,7 @@ km_status resort(km_ctx *c)
     p.X2 = c->X[nw]; p.a2 = c->a[nw]; p.u2 = c->u[nw]; p.perm2 = c->perm[nw];
     p.keys = c->keys; p.hist = c->hist; p.totals = c->totals; p.base = c->base;
     p.NL = c->NL; p.s = c->s; p.ks = c->ks;
-    p.lohist = getenv("KM_LINEAR_Q") ? nullptr : c->lohist;   // A/B: equal-width classes
+    p.lohist = c->lohist;
     p.qmap = c->qmap;
     p.n = c->n; p.k = c->k; p.DP = c->DP;
     p.Q = c->prune == KM_PRUNE_MTI ? c->Q : 1;
@@ -316,7 +320,7 @@ km_status resort(km_ctx *c)
 
 km_status allreduce(km_ctx *c)
 {
-    if (c->world <= 1) return KM_OK;   // global counters = local (iterate copies them once)
+    if (!c->comm_on) return KM_OK;   // global counters = local (iterate copies them once)
     NcclApi *N = nccl();
     if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable");
     ncclResult_t r;
@@ -337,6 +341,62 @@ float elapsed(cudaEvent_t a, cudaEvent_t b)
     return ms;
 }
 
+// event record that becomes an event node when the stream is being captured
+cudaError_t rec_event(cudaEvent_t e, cudaStream_t st) { return cudaEventRecordWithFlags(e, st, cudaEventRecordExternal); }
+
+// Everything of one iteration after any re-bucketing: S1 prep, S2+S3 pass, allreduce, S4 update,
+// copy of the counters to pinned host memory.  t >= 2 only.  Graph-capturable.
+km_status enqueue_body(km_ctx *c)
+{
+    cudaEvent_t *ev = c->ev;
+    KM_CUDA(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, c->st));
+    KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
+    KM_TRY(prep(c));
+    KM_CUDA(rec_event(ev[2], c->st));
+    KM_TRY(launch_assign(c, c->prune != KM_PRUNE_NONE ? km::MODE_MTI_REDUCE : km::MODE_DENSE_REDUCE, 0));
+    KM_CUDA(rec_event(ev[3], c->st));
+    KM_CUDA(rec_event(ev[4], c->st));
+    KM_TRY(allreduce(c));
+    KM_CUDA(rec_event(ev[5], c->st));
+    // the walk, tensor-core and TI passes reduce only the rows that moved (S += acc, reading B5);
+    // the knori- and legacy passes reduce every row (S = acc)
+    const int delta = (c->use_walk || c->use_tc || c->use_ti) ? 1 : 0;
+    KM_CUDA(km::launch_update(c->acc, c->S, delta, c->C, c->Cprev, c->k, c->d, c->DP,
+                              c->empty, c->spherical ? 1 : 0, c->st));
+    c->launches += 1;
+    static_assert(offsetof(HostStat, empty) == 8 * sizeof(unsigned long long), "HostStat layout");
+    KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long) + 2 * sizeof(int),
+                            cudaMemcpyDeviceToHost, c->st));
+    if (c->comm_on)
+        KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 8 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, c->st));
+    KM_CUDA(rec_event(ev[6], c->st));
+    return KM_OK;
+}
+
+// replay (capturing on first use) the graph of the body for the current row buffer
+km_status launch_body_graph(km_ctx *c)
+{
+    const int g = c->cur;
+    if (!c->gexec[g]) {
+        const int64_t l0 = c->launches;
+        KM_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        km_status s = enqueue_body(c);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+        if (s != KM_OK) { if (graph) cudaGraphDestroy(graph); return s; }
+        KM_CUDA(e);
+        e = cudaGraphInstantiate(&c->gexec[g], graph, 0);
+        cudaGraphDestroy(graph);
+        KM_CUDA(e);
+        c->glaunches[g] = c->launches - l0;
+        c->launches = l0;
+    }
+    KM_CUDA(cudaGraphLaunch(c->gexec[g], c->st));
+    c->launches += c->glaunches[g];
+    return KM_OK;
+}
+
 km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
 {
     KM_CUDA(cudaSetDevice(c->device));
@@ -355,19 +415,19 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
             // the bucket keys of iteration 1 come from the Forgy centroids' H; by iteration 3 the
             // centroids have settled, so the first re-bucketing is never later than t = 3
             need = (double)c->changed_since_sort > (double)c->resort_fraction * (double)c->n ||
-                   (c->t == 3 && c->last_sort_t == 1 && !getenv("KM_NO_T3_SORT"));
+                   (c->t == 3 && c->last_sort_t == 1);
         if (need) {
             KM_TRY(resort(c));
             sorted_now = true;
         }
     }
     KM_CUDA(cudaEventRecord(ev[1], c->st));
-    KM_CUDA(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, c->st));
-    KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
-    KM_TRY(prep(c));
-    KM_CUDA(cudaEventRecord(ev[2], c->st));
-    c->delta_pass = !first && (c->use_walk || c->use_tc || c->use_ti);
     if (first) {
+        // S0: dense pass, re-bucketing, full reduction of the sorted rows, update (S = acc)
+        KM_CUDA(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, c->st));
+        KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
+        KM_TRY(prep(c));
+        KM_CUDA(cudaEventRecord(ev[2], c->st));
         KM_TRY(launch_assign(c, km::MODE_DENSE, 0));
         KM_CUDA(cudaEventRecord(ev[3], c->st));
         if (c->resort_policy != KM_RESORT_NEVER) {
@@ -375,27 +435,26 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
             sorted_now = true;
         }
         KM_TRY(launch_assign(c, km::MODE_REDUCE_ONLY, 1));
-    } else {
-        KM_TRY(launch_assign(c, c->prune != KM_PRUNE_NONE ? km::MODE_MTI_REDUCE : km::MODE_DENSE_REDUCE, 0));
-        KM_CUDA(cudaEventRecord(ev[3], c->st));
-    }
-    KM_CUDA(cudaEventRecord(ev[4], c->st));
-    KM_TRY(allreduce(c));
-    KM_CUDA(cudaEventRecord(ev[5], c->st));
-    KM_CUDA(km::launch_update(c->acc, c->S, c->delta_pass ? 1 : 0, c->C, c->Cprev, c->k, c->d, c->DP, c->empty,
-                              c->spherical ? 1 : 0, c->st));
-    c->launches += 1;
-    static_assert(offsetof(HostStat, empty) == 8 * sizeof(unsigned long long), "HostStat layout");
-    // counters[8] and the ints that follow them (empty, ...) in one copy
-    KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long) + 2 * sizeof(int),
-                            cudaMemcpyDeviceToHost, c->st));
-    if (c->world > 1)
-        KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 8 * sizeof(unsigned long long),
+        KM_CUDA(cudaEventRecord(ev[4], c->st));
+        KM_TRY(allreduce(c));
+        KM_CUDA(cudaEventRecord(ev[5], c->st));
+        KM_CUDA(km::launch_update(c->acc, c->S, 0, c->C, c->Cprev, c->k, c->d, c->DP, c->empty,
+                                  c->spherical ? 1 : 0, c->st));
+        c->launches += 1;
+        KM_CUDA(cudaMemcpyAsync(c->hstat->local, c->counters, 8 * sizeof(unsigned long long) + 2 * sizeof(int),
                                 cudaMemcpyDeviceToHost, c->st));
-    KM_CUDA(cudaEventRecord(ev[6], c->st));
+        if (c->comm_on)
+            KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 8 * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, c->st));
+        KM_CUDA(cudaEventRecord(ev[6], c->st));
+    } else if (c->use_graph) {
+        KM_TRY(launch_body_graph(c));
+    } else {
+        KM_TRY(enqueue_body(c));
+    }
     KM_CUDA(cudaStreamSynchronize(c->st));
     HostStat *h = c->hstat;
-    if (c->world <= 1) memcpy(h->global, h->local, sizeof h->global);
+    if (!c->comm_on) memcpy(h->global, h->local, sizeof h->global);
     if (first) {
         rec.changed = c->n_global;
         rec.dists = c->n_global * (int64_t)c->k;
@@ -412,13 +471,9 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     rec.resorted = sorted_now;
     rec.ms_assign = elapsed(ev[2], ev[3]);
     rec.ms_sort = first ? elapsed(ev[3], ev[4]) : elapsed(ev[0], ev[1]);
-    rec.ms_comm = c->world > 1 ? elapsed(ev[4], ev[5]) : 0.f;
+    rec.ms_comm = c->comm_on ? elapsed(ev[4], ev[5]) : 0.f;
     rec.ms_iter = elapsed(ev[0], ev[6]);
     c->stats.push_back(rec);
-    if (getenv("KM_DEBUG"))
-        fprintf(stderr, "[km] t=%d changed=%lld dists=%lld clause1=%lld refined=%lld steps=%lld tc_walk=%llu tc_uncovered=%llu tc_misfit=%llu ms=%.3f/%.3f/%.3f\n",
-                c->t, (long long)rec.changed, (long long)rec.dists, (long long)rec.clause1, (long long)rec.refined,
-                (long long)rec.walk_steps, h->local[5], h->local[6], h->local[7], rec.ms_iter, rec.ms_assign, rec.ms_sort);
     if (changed_out) *changed_out = rec.changed;
     if (dists_out) *dists_out = rec.dists;
     return KM_OK;
@@ -435,6 +490,7 @@ void free_all(km_ctx *c)
     cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part); cudaFree(c->L); cudaFree(c->Hm);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
+    for (auto &g : c->gexec) if (g) cudaGraphExecDestroy(g);
     if (c->comm) { NcclApi *N = nccl(); if (N) N->CommDestroy(c->comm); }
     if (c->own_stream && c->st) cudaStreamDestroy(c->st);
 }
@@ -494,7 +550,6 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     // prefix classes per cluster: up to 32 while k*Q <= KM_NB_MAX bucket cursors (scatter smem)
     // (k = 100 and k = 1000: 32 classes of equal population)
     c->Q = std::max(1, std::min(32, KM_NB_MAX / k));
-    if (const char *e = getenv("KM_Q")) c->Q = std::max(1, std::min(KM_NB_MAX / k, atoi(e)));   // A/B
     const int NBmax = k * c->Q;
     c->ntiles = (int)((n + c->tile_rows - 1) / c->tile_rows);
     KM_TRY(dalloc(&c->keys, (size_t)n));
@@ -579,17 +634,13 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     // AUTO: the CUDA-core walk (measured faster than the tensor-core pipeline on C3 and C4 so
     // far); KM_ENGINE_TENSOR selects the tcgen05 kernel
     c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 && !c->use_ti &&
-                (o->engine == KM_ENGINE_TENSOR || (o->engine == KM_ENGINE_AUTO && getenv("KM_AUTO_TC")));
+                o->engine == KM_ENGINE_TENSOR;
     if (o->engine == KM_ENGINE_TENSOR && !km::tc_supported(DP))
         return fail(KM_EARG, "tensor engine needs d padded to 8, 16 or 32 (d=%d)", d);
-    if (const char *e = getenv("KM_ENGINE")) {
-        if (!strcmp(e, "cuda")) c->use_tc = false;
-    }
     // the tensor-core kernel handles rows outside the tile's cluster without extra walks, so
     // re-bucketing only pays when the layout is badly mixed
     if (c->use_tc) {
         c->tc_nmax = std::min(256, std::max(16, (k - 1 + 15) & ~15));   // columns: NL[A] prefix
-        if (const char *e = getenv("KM_TC_NMAX")) c->tc_nmax = std::max(16, std::min(c->tc_nmax, atoi(e) & ~15));
         if (km::tc_plan(DP, c->csmem, k, c->tc_nmax, c->num_sms, &c->tc_grid, &c->tc_cols) == 0) {
             if (o->engine == KM_ENGINE_TENSOR)
                 return fail(KM_EARG, "tensor engine: shared memory for d=%d k=%d exceeds one SM", d, k);
@@ -602,8 +653,8 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         KM_TRY(dalloc(&c->Bmeta, (size_t)k * km::tc_nmeta_host(c->tc_nmax)));
         c->part_grid = std::max(c->part_grid, c->tc_grid);
     }
-    // CUDA-core engine: the centred expansion-form walk (k_walk); KM_LEGACY_WALK=1 keeps the
-    // direct-form lane walk of k_assign for A/B comparison
+    // CUDA-core engine: the centred expansion-form walk (k_walk); KM_ENGINE_CUDA_CORE with a
+    // compile-time -DKM_LEGACY_WALK keeps the direct-form lane walk of k_assign (A/B builds only)
     if (c->use_ti) {
         // Elkan's O(nk) lower-bound matrix: fp32, centroid-major
         const size_t lbytes = (size_t)k * c->n_alloc * sizeof(float);
@@ -614,15 +665,18 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         c->ti_grid = km::ti_grid(DP, c->csmem, k, c->num_sms);
         c->part_grid = std::max(c->part_grid, c->ti_grid);
     }
-    c->use_walk = !c->use_tc && !c->use_ti && c->prune == KM_PRUNE_MTI && k >= 2 && km::walk_supported(DP) &&
-                  !getenv("KM_LEGACY_WALK");
+#ifdef KM_LEGACY_WALK
+    c->use_walk = false;
+#else
+    c->use_walk = !c->use_tc && !c->use_ti && c->prune == KM_PRUNE_MTI && k >= 2 && km::walk_supported(DP);
+#endif
     if (c->use_walk) {
         c->wpad = (k + 1) & ~1;                    // k-1 neighbours + >= 1 dummy row, even
         c->wbits = 1;
         while ((1 << c->wbits) < c->wpad) ++c->wbits;
         c->whs = 16;
         while (c->whs < c->wpad) c->whs <<= 1;
-        c->wh_smem = c->whs <= 256 && (size_t)k * c->whs * sizeof(float) <= 56 * 1024 && !getenv("KM_WH_GLOBAL");
+        c->wh_smem = c->whs <= 256 && (size_t)k * c->whs * sizeof(float) <= 56 * 1024;
         if (!c->wh_smem && c->whs < 256) c->whs = 256;
         KM_TRY(dalloc(&c->Wblk, (size_t)k * (c->wpad / 2) * (DP / 2)));
         KM_TRY(dalloc(&c->Wcc, (size_t)k * c->wpad));
@@ -641,7 +695,9 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     if ((c->use_tc || c->use_walk) && !(o->resort_fraction > 0.f)) c->resort_fraction = 0.25f;
     c->nslab = std::min(c->part_grid, c->num_sms);
     KM_TRY(dalloc(&c->acc_part, (size_t)c->nslab * k * (DP + 1)));
-    if (c->world > 1) {
+    c->use_graph = o->no_graph == 0;
+    c->comm_on = c->world > 1 || o->force_comm != 0;
+    if (c->comm_on) {
         NcclApi *N = nccl();
         if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable (world=%d)", c->world);
         ncclUniqueId id;
@@ -804,7 +860,7 @@ km_status kmeans_sse(km_ctx *c, double *out)
     KM_CUDA(cudaMemsetAsync(c->sse_buf, 0, sizeof(double), c->st));
     KM_CUDA(km::launch_sse(c->X[c->cur], c->a[c->cur], c->C, c->n, c->d, c->DP, c->sse_buf, c->st));
     c->launches += 1;
-    if (c->world > 1) {
+    if (c->comm_on) {
         NcclApi *N = nccl();
         if (!N) return fail(KM_ENCCL, "libnccl.so.2 not loadable");
         ncclResult_t r = N->AllReduce(c->sse_buf, c->sse_buf, 1, ncclFloat64, ncclSum, c->comm, c->st);

@@ -122,8 +122,8 @@ int walk_grid(int DP, bool csmem, int k, int kp, bool whs, int num_sms);
 cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int kp, int whs,
                              float4 *Wblk, float *Wcc, float2 *Wmeta, float *WH, cudaStream_t st);
 int ti_grid(int DP, bool csmem, int k, int num_sms);
-cudaError_t launch_ti(int DP, bool csmem, bool first, const AssignParams &p, float *L, int64_t ldl,
-                      const float *Hm, int grid, cudaStream_t st);
+cudaError_t launch_ti(int DP, bool csmem, bool first, const AssignParams &p, float *L, const float *Hm, int grid,
+                      cudaStream_t st);
 cudaError_t launch_prep_ti(const uint64_t *NL, int k, int ks, float *Hm, cudaStream_t st);
 cudaError_t launch_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
                           int DP, int *empty, int spherical, cudaStream_t st);

@@ -758,9 +758,6 @@ size_t tc_plan(int DP, bool csmem, int k, int nmax, int num_sms, int *grid, int 
     ctas = std::min(ctas, 512 / cols);
     *tmem_cols = cols;
     *grid = std::max(1, ctas) * num_sms;
-    if (getenv("KM_DEBUG"))
-        fprintf(stderr, "[km] tc plan: DP=%d k=%d nmax=%d S=%d NA=%d NB=%d smem=%d cols=%d ctas/SM=%d\n",
-                DP, k, nmax, L.S, L.NA, L.NB, L.total, cols, ctas);
     return ctas > 0 ? (size_t)L.total : 0;
 }
 

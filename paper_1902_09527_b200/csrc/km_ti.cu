@@ -12,9 +12,10 @@
 //       if still u > l[c] and u > H[best][c]: l[c] = d(x, c) (1 distance); c closer -> best = c, u = d
 //
 // B200 realisation.  One lane = one row, rows in the caller's order (TI keeps an n x k matrix
-// per row, so the rows are never re-bucketed); the lower bounds are stored centroid-major,
-// L[c * n_alloc + i], so for every c the 32 lanes of a warp read and write one coalesced 128-B
-// line: the pass is bound by the 8 k bytes per row of lower-bound traffic (the O(nk)
+// per row, so the rows are never re-bucketed); the lower bounds are stored centroid-major within
+// 32-row groups, so for every c the 32 lanes of a warp read and write one coalesced 128-B
+// line — and the k lines of a 32-row group are contiguous (L[((i / 32) k + c) 32 + i % 32], so a warp
+// streams one 128 k-byte block): the pass is bound by the 8 k bytes per row of lower-bound traffic (the O(nk)
 // maintenance cost the paper attributes to TI).  Exact mode as in the MTI
 // engines: bounds in fp32 with directed rounding (l rounded down, u up, H down), so every prune
 // is sound; the winner among the evaluated candidates is certified by the top-2 intervals or
@@ -28,10 +29,14 @@
 namespace km {
 
 constexpr int kTiThreads = 256;
+constexpr int kTiBatch = 8;      // lower bounds loaded per batch (loads in flight per lane)
+
+// resident CTAs per SM requested from ptxas (registers): 4 (64 registers) up to d = 16, 3 at 32
+template <int DP> constexpr int ti_min_blocks() { return DP <= 16 ? 4 : (DP <= 32 ? 3 : 2); }
 
 template <int DP, bool CSMEM, bool HSMEM, bool FIRST>
-__global__ void __launch_bounds__(kTiThreads)
-k_ti(AssignParams p, float *__restrict__ L, int64_t ldl, const float *__restrict__ Hm)
+__global__ void __launch_bounds__(kTiThreads, ti_min_blocks<DP>())
+k_ti(AssignParams p, float *__restrict__ L, const float *__restrict__ Hm)
 {
     extern __shared__ __align__(16) float smem[];
     const int k = p.k;
@@ -72,7 +77,7 @@ k_ti(AssignParams p, float *__restrict__ L, int64_t ldl, const float *__restrict
                 x[4 * j] = t.x; x[4 * j + 1] = t.y; x[4 * j + 2] = t.z; x[4 * j + 3] = t.w;
             }
         }
-        float *Lr = L + row;
+        float *Lr = L + (base >> 5) * (int64_t)k * 32 + lane;   // bound c of this row: Lr[32 c]
         int anew;
         float unew;
         if constexpr (FIRST) {
@@ -81,7 +86,7 @@ k_ti(AssignParams p, float *__restrict__ L, int64_t ldl, const float *__restrict
             int bc = 0;
             for (int c = 0; c < k; ++c) {
                 const float q = dist2<DP, CSMEM>(x, Cn, c);
-                if (valid) Lr[(int64_t)c * ldl] = lower_d(q, p.g_dn, eps);
+                if (valid) Lr[32 * c] = lower_d(q, p.g_dn, eps);
                 q2 = fminf(q2, fmaxf(q, bq));
                 bc = q < bq ? c : bc;
                 bq = fminf(q, bq);
@@ -102,28 +107,39 @@ k_ti(AssignParams p, float *__restrict__ L, int64_t ldl, const float *__restrict
             int best = a0;
             float bq = INFINITY, q2 = INFINITY, la = 0.f, ut = 0.f;
             unsigned nd = 0;
-            for (int c = 0; c < k; ++c) {
-                float l = valid ? fmaxf(0.f, __fsub_rd(Lr[(int64_t)c * ldl], sF[c])) : 0.f;
-                if (tight && c == a0) l = la;
-                if (live && c != best && ub > l && ub > H[best * k + c]) {
-                    if (!tight) {                    // Elkan step 3a: u = d(x, C[a0]), once
-                        bq = dist2<DP, CSMEM>(x, Cn, a0);
-                        ub = upper_d(bq, p.g_up, eps);
-                        ut = ub;
-                        la = lower_d(bq, p.g_dn, eps);
-                        tight = true;
-                        ++nd;
-                        if (a0 < c) Lr[(int64_t)a0 * ldl] = la;   // already written this pass
+            // the lower bounds are streamed kTiBatch at a time (independent loads in flight:
+            // the pass is bound by this O(nk) traffic)
+            for (int c0 = 0; c0 < k; c0 += kTiBatch) {
+                float lb[kTiBatch];
+#pragma unroll
+                for (int j = 0; j < kTiBatch; ++j)
+                    lb[j] = (valid && c0 + j < k) ? __ldcs(Lr + 32 * (c0 + j)) : 0.f;
+#pragma unroll
+                for (int j = 0; j < kTiBatch; ++j) {
+                    const int c = c0 + j;
+                    if (c >= k) break;
+                    float l = fmaxf(0.f, __fsub_rd(lb[j], sF[c]));
+                    if (tight && c == a0) l = la;
+                    if (live && c != best && ub > l && ub > H[best * k + c]) {
+                        if (!tight) {                    // Elkan step 3a: u = d(x, C[a0]), once
+                            bq = dist2<DP, CSMEM>(x, Cn, a0);
+                            ub = upper_d(bq, p.g_up, eps);
+                            ut = ub;
+                            la = lower_d(bq, p.g_dn, eps);
+                            tight = true;
+                            ++nd;
+                            if (a0 < c) Lr[32 * a0] = la;   // already written this pass
+                        }
+                        if (ub > l && ub > H[best * k + c]) {     // step 3b with the tightened u
+                            const float q = dist2<DP, CSMEM>(x, Cn, c);
+                            ++nd;
+                            l = lower_d(q, p.g_dn, eps);
+                            q2 = fminf(q2, fmaxf(q, bq));
+                            if (q < bq) { bq = q; best = c; ub = upper_d(q, p.g_up, eps); }
+                        }
                     }
-                    if (ub > l && ub > H[best * k + c]) {     // step 3b with the tightened u
-                        const float q = dist2<DP, CSMEM>(x, Cn, c);
-                        ++nd;
-                        l = lower_d(q, p.g_dn, eps);
-                        q2 = fminf(q2, fmaxf(q, bq));
-                        if (q < bq) { bq = q; best = c; ub = upper_d(q, p.g_up, eps); }
-                    }
+                    if (valid) __stcs(Lr + 32 * c, l);
                 }
-                if (valid) Lr[(int64_t)c * ldl] = l;
             }
             anew = best;
             unew = ub;
@@ -183,7 +199,7 @@ static size_t ti_smem(int DP, bool csmem, bool hsmem, int k)
 
 bool ti_h_smem(int DP, bool csmem, int k) { return ti_smem(DP, csmem, true, k) <= 200 * 1024; }
 
-typedef void (*ti_kernel_t)(AssignParams, float *, int64_t, const float *);
+typedef void (*ti_kernel_t)(AssignParams, float *, const float *);
 
 template <int DP>
 static ti_kernel_t ti_pick(bool cs, bool hs, bool first)
@@ -229,8 +245,8 @@ int ti_grid(int DP, bool csmem, int k, int num_sms)
     return best;
 }
 
-cudaError_t launch_ti(int DP, bool csmem, bool first, const AssignParams &p, float *L, int64_t ldl,
-                      const float *Hm, int grid, cudaStream_t st)
+cudaError_t launch_ti(int DP, bool csmem, bool first, const AssignParams &p, float *L, const float *Hm, int grid,
+                      cudaStream_t st)
 {
     const bool hs = ti_h_smem(DP, csmem, p.k);
     ti_kernel_t kern = ti_kernel(DP, csmem, hs, first);
@@ -240,7 +256,7 @@ cudaError_t launch_ti(int DP, bool csmem, bool first, const AssignParams &p, flo
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, kTiThreads, sm, st>>>(p, L, ldl, Hm);
+    kern<<<grid, kTiThreads, sm, st>>>(p, L, Hm);
     return cudaGetLastError();
 }
 

@@ -37,7 +37,8 @@ class KMeans:
     def __init__(self, points, init_centroids, *, prune: str = "mti", device: Optional[int] = None,
                  stream=None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  n_global: int = 0, check_finite: bool = False, resort: str = "auto",
-                 resort_fraction: float = 0.0, engine: str = "auto", spherical: bool = False):
+                 resort_fraction: float = 0.0, engine: str = "auto", spherical: bool = False,
+                 graph: bool = True, force_comm: bool = False):
         L = C.lib()
         o = default_options()
         self._keep = []
@@ -80,6 +81,8 @@ class KMeans:
         o.engine = {"auto": C.KM_ENGINE_AUTO, "cuda": C.KM_ENGINE_CUDA_CORE,
                     "tensor": C.KM_ENGINE_TENSOR}[engine]
         o.spherical = int(bool(spherical))
+        o.no_graph = int(not graph)
+        o.force_comm = int(bool(force_comm))
         h = ct.c_void_p()
         C.check(L.kmeans_create(n, d, C0.shape[0], ptr, C0.ctypes.data, ct.byref(o), ct.byref(h)))
         self._h = h

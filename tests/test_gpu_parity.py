@@ -338,3 +338,73 @@ def test_skmeans_and_seed_odd_shapes(d, k):
     g = gpu_run(X, C_g, 50, "mti", spherical=True)
     assert g["iterations"] == r.iterations and np.array_equal(g["a"], r.a)
     assert centroid_rel_err(g["C"], r.C).max() <= 1e-12
+
+
+# ---- CUDA graph replay and the collective path ------------------------------------
+def test_graph_replay_equals_eager():
+    """Iterations t >= 2 replayed from a captured CUDA graph (default) give the same assignments,
+    centroids and per-iteration counts as eager launches, across re-bucketing (both row buffers)."""
+    X, idx, _ = make_config("c3", n=400_000)
+    C0 = X[idx].astype(float)
+    g = gpu_run(X, C0, 20, "mti")
+    e = gpu_run(X, C0, 20, "mti", graph=False)
+    assert g["iterations"] == e["iterations"] and np.array_equal(g["a"], e["a"])
+    assert np.array_equal(g["C"], e["C"])
+    for f in ("changed", "dists", "clause1", "empty", "resorted"):
+        assert [s[f] for s in g["stats"]] == [s[f] for s in e["stats"]], f
+    assert sum(s["resorted"] for s in g["stats"][1:]) >= 1
+
+
+def test_nccl_path_at_world_1():
+    """The library's NCCL data path (communicator from a fresh ncclUniqueId, one allreduce of
+    [sums | counts] and the counters per iteration, captured in the iteration graph; SSE
+    allreduce) on a 1-rank communicator: strict parity with the oracle."""
+    from paper_1902_09527_b200 import nccl_unique_id
+    X, idx, _ = make_config("c2")
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, 50, 0, "mti")
+    for graph in (True, False):
+        g = gpu_run(X, C0, 50, "mti", nccl_id=nccl_unique_id(), force_comm=True, graph=graph)
+        assert_strict(g, r)
+        assert all(s["ms_comm"] > 0 for s in g["stats"])
+
+
+def _two_gpu_worker(rank, port, X, C0, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=2)
+    from paper_1902_09527_b200 import KMeans as KM, nccl_unique_id
+    from paper_1902_09527_b200.dist import broadcast_bytes, shard_bounds
+    lo, hi = shard_bounds(X.shape[0], rank, 2)
+    nid = broadcast_bytes(nccl_unique_id() if rank == 0 else b"\0" * 128)
+    km = KM(torch.from_numpy(X[lo:hi]).cuda(), C0, rank=rank, world=2, nccl_id=nid, n_global=X.shape[0])
+    it, _ = km.run(50, 0)
+    q.put((rank, it, km.assignments(), km.centroids(), km.sse()))
+    km.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_two_gpus_equal_one():
+    """G = 2 contiguous shards (§7) vs G = 1: same iterations and assignments, centroids
+    bitwise identical on both ranks and <= 1e-12 from G = 1 (only the fp64 reduction order differs)."""
+    import socket
+    import torch.multiprocessing as mp
+    X, idx, _ = make_config("c2")
+    C0 = X[idx].astype(float)
+    one = gpu_run(X, C0, 50, "mti")
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_two_gpu_worker, args=(r, port, X, C0, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    (_, it0, a0, Ca, s0), (_, it1, a1, Cb, s1) = res
+    assert it0 == it1 == one["iterations"]
+    assert np.array_equal(np.concatenate([a0, a1]), one["a"])
+    assert np.array_equal(Ca, Cb) and centroid_rel_err(Ca, one["C"]).max() <= 1e-12
+    assert s0 == s1 and abs(s0 - one["sse"]) <= 1e-12 * one["sse"]

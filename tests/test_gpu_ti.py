@@ -72,7 +72,10 @@ def test_ti_free_running_strict(name, n, iters):
     assert abs(g["sse"] - r.final_sse) <= 1e-12 * r.final_sse
     assert [s["changed"] for s in g["stats"]] == r.changed.tolist()
     gd = np.array([s["dists"] for s in g["stats"]])
-    assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists + 2), (gd.tolist(), r.dists.tolist())
+    # soft check: 0.1 % relative, plus borderline rows (bound tests within the fp32 rounding margin
+    # go either way; their number scales with n, not with the count: 1 per 100k rows)
+    tol = 1e-3 * r.dists + 1e-5 * X.shape[0] + 2
+    assert np.all(np.abs(gd - r.dists) <= tol), (gd.tolist(), r.dists.tolist())
     # TI's bounds only remove computations: fewer distances than MTI (same trajectory)
     m = run(X, C0, iters, "mti")
     md = np.array([s["dists"] for s in m["stats"]])
