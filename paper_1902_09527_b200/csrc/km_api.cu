@@ -342,7 +342,14 @@ float elapsed(cudaEvent_t a, cudaEvent_t b)
 }
 
 // event record that becomes an event node when the stream is being captured
-cudaError_t rec_event(cudaEvent_t e, cudaStream_t st) { return cudaEventRecordWithFlags(e, st, cudaEventRecordExternal); }
+cudaError_t rec_event(cudaEvent_t e, cudaStream_t st)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t err = cudaStreamIsCapturing(st, &cs);
+    if (err != cudaSuccess) return err;
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, st);
+}
 
 // Everything of one iteration after any re-bucketing: S1 prep, S2+S3 pass, allreduce, S4 update,
 // copy of the counters to pinned host memory.  t >= 2 only.  Graph-capturable.
