@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats-out", default=None)
+    ap.add_argument("--engine", default="auto", choices=["auto", "cuda", "tensor"],
+                    help="MTI pass engine (auto = the CUDA-core walk k_walk)")
+    ap.add_argument("--resort-fraction", type=float, default=0.0)
     ap.add_argument("--no-graph", action="store_true", help="launch each iteration eagerly (no CUDA graph)")
     ap.add_argument("--force-comm", action="store_true",
                     help="run the NCCL allreduce even at N = 1 (1-rank communicator)")
@@ -245,7 +248,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     km = KMeans(Xd, C0, prune=args.prune, stream=stream.cuda_stream, rank=rank, world=world,
                 spherical=args.algo == "skmeans", graph=not args.no_graph, force_comm=args.force_comm,
-                nccl_id=nccl_id, n_global=n)
+                engine=args.engine, resort_fraction=args.resort_fraction, nccl_id=nccl_id, n_global=n)
     for _ in range(args.warmup):
         km.iterate()
     launches0 = km.launch_count
@@ -337,6 +340,7 @@ def run_ours(args, rank, world, local_rank):
             t0 = time.perf_counter()
             km2 = KMeans(Xh, C0, prune=args.prune, rank=rank, world=world, nccl_id=nid, n_global=n,
                          spherical=args.algo == "skmeans", graph=not args.no_graph, force_comm=args.force_comm,
+                         engine=args.engine, resort_fraction=args.resort_fraction,
                          device=local_rank)
             t1 = time.perf_counter()
             for _ in range(total_iters):

@@ -91,7 +91,12 @@ typedef struct km_options {
     int32_t force_comm;        /* 1 = create the NCCL communicator and run the allreduce even when
                                   world == 1 (a 1-rank communicator; needs nccl_unique_id): exercises
                                   the multi-GPU data path on one GPU */
-    int32_t reserved[4];
+    float resum_moves;         /* the walk, tensor-core and TI passes update the per-cluster sums by the
+                                  rows that moved (reading B5); once the moves applied since
+                                  the last full reduction exceed resum_moves * n_global, the sums are
+                                  re-derived from every row (bounds fp64 drift).  0 = default 4;
+                                  < 0 = never */
+    int32_t reserved[3];
 } km_options;
 
 typedef struct km_iter_stats {

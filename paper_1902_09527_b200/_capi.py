@@ -28,7 +28,7 @@ class KmOptions(ct.Structure):
                 ("check_finite", ct.c_int32), ("points_on_host", ct.c_int32),
                 ("resort_policy", ct.c_int32), ("resort_fraction", ct.c_float),
                 ("engine", ct.c_int32), ("spherical", ct.c_int32), ("no_graph", ct.c_int32),
-                ("force_comm", ct.c_int32), ("reserved", ct.c_int32 * 4)]
+                ("force_comm", ct.c_int32), ("resum_moves", ct.c_float), ("reserved", ct.c_int32 * 3)]
 
 
 class KmIterStats(ct.Structure):

@@ -181,6 +181,8 @@ struct km_ctx {
     float *L = nullptr, *Hm = nullptr;
     int ti_grid = 0;
     size_t dev_bytes = 0;           // device memory held by the context
+    double resum_moves = 4.0;       // full re-summation once moves since the last one > this * n_global
+    int64_t moves_since_full = 0;   // global moves applied as deltas since the last full reduction
     std::vector<km_iter_stats> stats;
     cudaEvent_t ev[7] = {};
     ncclComm_t comm = nullptr;
@@ -352,8 +354,9 @@ cudaError_t rec_event(cudaEvent_t e, cudaStream_t st)
 }
 
 // Everything of one iteration after any re-bucketing: S1 prep, S2+S3 pass, allreduce, S4 update,
-// copy of the counters to pinned host memory.  t >= 2 only.  Graph-capturable.
-km_status enqueue_body(km_ctx *c)
+// copy of the counters to pinned host memory.  t >= 2 only.  Graph-capturable.  full: after the
+// pass, re-derive the per-cluster sums from every row (instead of adding this pass's moves).
+km_status enqueue_body(km_ctx *c, bool full = false)
 {
     cudaEvent_t *ev = c->ev;
     KM_CUDA(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, c->st));
@@ -362,12 +365,16 @@ km_status enqueue_body(km_ctx *c)
     KM_CUDA(rec_event(ev[2], c->st));
     KM_TRY(launch_assign(c, c->prune != KM_PRUNE_NONE ? km::MODE_MTI_REDUCE : km::MODE_DENSE_REDUCE, 0));
     KM_CUDA(rec_event(ev[3], c->st));
+    if (full) {
+        KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
+        KM_TRY(launch_assign(c, km::MODE_REDUCE_ONLY, 1));
+    }
     KM_CUDA(rec_event(ev[4], c->st));
     KM_TRY(allreduce(c));
     KM_CUDA(rec_event(ev[5], c->st));
     // the walk, tensor-core and TI passes reduce only the rows that moved (S += acc, reading B5);
     // the knori- and legacy passes reduce every row (S = acc)
-    const int delta = (c->use_walk || c->use_tc || c->use_ti) ? 1 : 0;
+    const int delta = (c->use_walk || c->use_tc || c->use_ti) && !full ? 1 : 0;
     KM_CUDA(km::launch_update(c->acc, c->S, delta, c->C, c->Cprev, c->k, c->d, c->DP,
                               c->empty, c->spherical ? 1 : 0, c->st));
     c->launches += 1;
@@ -454,10 +461,18 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
             KM_CUDA(cudaMemcpyAsync(c->hstat->global, c->counters_g, 8 * sizeof(unsigned long long),
                                     cudaMemcpyDeviceToHost, c->st));
         KM_CUDA(cudaEventRecord(ev[6], c->st));
-    } else if (c->use_graph) {
-        KM_TRY(launch_body_graph(c));
     } else {
-        KM_TRY(enqueue_body(c));
+        // the decision uses global counts only, so every rank takes it in the same iteration
+        const bool full = (c->use_walk || c->use_tc || c->use_ti) && c->resum_moves >= 0.0 &&
+                          (double)c->moves_since_full > c->resum_moves * (double)c->n_global;
+        if (full) {
+            KM_TRY(enqueue_body(c, true));
+            c->moves_since_full = 0;
+        } else if (c->use_graph) {
+            KM_TRY(launch_body_graph(c));
+        } else {
+            KM_TRY(enqueue_body(c));
+        }
     }
     KM_CUDA(cudaStreamSynchronize(c->st));
     HostStat *h = c->hstat;
@@ -470,6 +485,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
         rec.changed = (int64_t)h->global[0];
         rec.dists = (int64_t)h->global[1];
         c->changed_since_sort += (int64_t)h->local[0];
+        c->moves_since_full += rec.changed;
     }
     rec.clause1 = (int64_t)h->global[2];
     rec.refined = (int64_t)h->global[3];
@@ -703,6 +719,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     c->nslab = std::min(c->part_grid, c->num_sms);
     KM_TRY(dalloc(&c->acc_part, (size_t)c->nslab * k * (DP + 1)));
     c->use_graph = o->no_graph == 0;
+    c->resum_moves = o->resum_moves == 0.f ? 4.0 : (double)o->resum_moves;
     c->comm_on = c->world > 1 || o->force_comm != 0;
     if (c->comm_on) {
         NcclApi *N = nccl();

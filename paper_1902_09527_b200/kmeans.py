@@ -38,7 +38,7 @@ class KMeans:
                  stream=None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  n_global: int = 0, check_finite: bool = False, resort: str = "auto",
                  resort_fraction: float = 0.0, engine: str = "auto", spherical: bool = False,
-                 graph: bool = True, force_comm: bool = False):
+                 graph: bool = True, force_comm: bool = False, resum_moves: float = 0.0):
         L = C.lib()
         o = default_options()
         self._keep = []
@@ -83,6 +83,7 @@ class KMeans:
         o.spherical = int(bool(spherical))
         o.no_graph = int(not graph)
         o.force_comm = int(bool(force_comm))
+        o.resum_moves = float(resum_moves)
         h = ct.c_void_p()
         C.check(L.kmeans_create(n, d, C0.shape[0], ptr, C0.ctypes.data, ct.byref(o), ct.byref(h)))
         self._h = h

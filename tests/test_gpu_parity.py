@@ -408,3 +408,30 @@ def test_two_gpus_equal_one():
     assert np.array_equal(np.concatenate([a0, a1]), one["a"])
     assert np.array_equal(Ca, Cb) and centroid_rel_err(Ca, one["C"]).max() <= 1e-12
     assert s0 == s1 and abs(s0 - one["sse"]) <= 1e-12 * one["sse"]
+
+
+def test_periodic_full_resummation():
+    """Running sums updated by deltas (reading B5) are re-derived from every row once the moves
+    since the last full reduction exceed resum_moves * n: with a tiny threshold (a full
+    reduction almost every iteration) the run is still strict-parity with the oracle."""
+    X, idx, _ = make_config("c2")
+    C0 = X[idx].astype(float)
+    r = oracle.lloyd(X, C0, 50, 0, "mti")
+    assert_strict(gpu_run(X, C0, 50, "mti", resum_moves=0.01), r)
+
+
+def test_long_run_delta_sums_do_not_drift():
+    """200 iterations of C2 with delta sums only (no re-summation): the centroids stay within
+    1e-12 of the oracle's means of the GPU's own assignments (fp64 rounding of ~1e6 moves)."""
+    X, idx, _ = make_config("c2")
+    C0 = X[idx].astype(float)
+    Xd = torch.from_numpy(X).cuda()
+    km = KMeans(Xd, C0, prune="mti", resum_moves=-1.0)
+    it, _ = km.run(200, 0)
+    a = km.assignments()
+    sums, counts = oracle.cluster_sums(X, a, 100)
+    C_means, _ = oracle.update(sums, counts, km.centroids())
+    assert centroid_rel_err(km.centroids(), C_means).max() <= 1e-12
+    moved = sum(s["changed"] for s in km.stats()[1:])
+    assert moved > 0
+    km.close()
