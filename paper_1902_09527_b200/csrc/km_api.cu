@@ -100,6 +100,10 @@ struct HostStat {
     unsigned long long global[8];  // after allreduce (world 1: = local)
 };
 
+// clause-1 rate above which the walk stages only the rows that fail clause 1 (SKIP1): C5 (0.29 ->
+// 0.42), C2 (0.16 -> 0.46) and C1 (0.45) use it, C3 (<= 0.04) and C4 (<= 0.01) do not
+constexpr double kSkip1Rate = 0.15;
+
 int pad_dim(int d)
 {
     for (int p : {4, 8, 16, 32, 64})
@@ -189,8 +193,11 @@ struct km_ctx {
     bool comm_on = false;           // allreduce runs (world > 1, or force_comm)
     // CUDA graph of one iteration t >= 2 (S1-S4 + allreduce + counter copy), one per row buffer
     bool use_graph = true;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    int64_t glaunches[2] = {0, 0};  // kernels in each graph
+    cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};   // [row buffer][skip1]
+    int64_t glaunches[4] = {0, 0, 0, 0};   // kernels in each graph
+    // NEXT-2: the walk reads only the rows that fail clause 1, chosen when the last pass's
+    // clause-1 rate exceeded kSkip1Rate (global counts: the same choice on every rank)
+    bool skip1 = false;
     int64_t launches = 0;
 };
 
@@ -278,7 +285,7 @@ km_status launch_assign(km_ctx *c, int mode, int work_slot)
         KM_CUDA(km::launch_ti(c->DP, c->csmem, mode == km::MODE_DENSE, p, c->L, c->Hm, c->ti_grid, c->st));
     } else if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
         if (c->use_tc) KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
-        else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->st));
+        else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->skip1, c->st));
         if (c->use_tc || !c->wh_smem) {   // deferred distance counts (misfit rows)
             KM_CUDA(km::launch_mti_count(c->defer, c->dcount, c->n_alloc / 128, c->counters, c->NL, c->ks, c->k,
                                          c->num_sms, c->st));
@@ -391,7 +398,7 @@ km_status enqueue_body(km_ctx *c, bool full = false)
 // replay (capturing on first use) the graph of the body for the current row buffer
 km_status launch_body_graph(km_ctx *c)
 {
-    const int g = c->cur;
+    const int g = c->cur * 2 + (c->skip1 ? 1 : 0);
     if (!c->gexec[g]) {
         const int64_t l0 = c->launches;
         KM_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
@@ -488,6 +495,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
         c->moves_since_full += rec.changed;
     }
     rec.clause1 = (int64_t)h->global[2];
+    c->skip1 = (double)rec.clause1 > kSkip1Rate * (double)c->n_global;
     rec.refined = (int64_t)h->global[3];
     rec.walk_steps = (int64_t)h->global[4];
     rec.empty = h->empty;

@@ -117,7 +117,7 @@ cudaError_t launch_mti_count(const unsigned long long *defer, const int *dcount,
                              cudaStream_t st);
 int tc_nmeta_host(int nmax);
 bool walk_supported(int DP);
-cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st);
+cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, bool skip1, cudaStream_t st);
 int walk_grid(int DP, bool csmem, int k, int kp, bool whs, int num_sms);
 cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int kp, int whs,
                              float4 *Wblk, float *Wcc, float2 *Wmeta, float *WH, cudaStream_t st);
