@@ -169,6 +169,24 @@ __host__ __device__ constexpr int walk_threads_of(int DP)
 template <int DP> constexpr int walk_threads() { return walk_threads_of(DP); }
 static int walk_threads_rt(int DP) { return walk_threads_of(DP); }
 
+// Staged row r, 16-byte part q (of DP/4) lives in float4 slot r (DP/4) + (q ^ g(r)): the lanes of
+// a warp read part q of rows lane, lane + 32 with one LDS.128 each, and without the swizzle rows
+// DP*4 bytes apart fall on the same banks (DP = 32: an 8-way conflict per quarter warp; ncu of
+// C4: 474M shared bank conflicts, L1 throughput 88 %).  g spreads 8 consecutive rows over the 8
+// 16-byte bank groups.
+#ifndef KM_SWZ_MIN_DP
+#define KM_SWZ_MIN_DP 16      // DP = 8 rows (32 B) conflict only 2-way; measured separately
+#endif
+template <int DP>
+__device__ __forceinline__ int stg_swz(int c)
+{
+    constexpr int P = DP / 4;                     // parts per row
+    if constexpr (DP < KM_SWZ_MIN_DP) return c;
+    const int r = c / P, q = c % P;
+    const int g = P >= 8 ? (r & 7) : ((r * P) >> 3) & (P - 1);
+    return r * P + (q ^ g);
+}
+
 #define KM_WALK_NAME k_walk
 #define KM_SKIP1 0
 #include "km_walk_body.cuh"

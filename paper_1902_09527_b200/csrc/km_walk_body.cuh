@@ -108,7 +108,7 @@ KM_WALK_NAME(AssignParams p)
         float4 *xd = reinterpret_cast<float4 *>(stg);
 #pragma unroll
         for (int c = lane; c < kRowsB * DP / 4; c += 32)
-            if ((live >> (c / (DP / 4))) & 1ull) cp_async16(xd + c, xs + c);
+            if ((live >> (c / (DP / 4))) & 1ull) cp_async16(xd + stg_swz<DP>(c), xs + c);
     };
     int chunk_row = n;
 #else
@@ -120,7 +120,7 @@ KM_WALK_NAME(AssignParams p)
         const float4 *xs = reinterpret_cast<const float4 *>(p.X + (size_t)r0 * DP);
         float4 *xd = reinterpret_cast<float4 *>(stg);
 #pragma unroll
-        for (int c = lane; c < kRowsB * DP / 4; c += 32) cp_async16(xd + c, xs + c);
+        for (int c = lane; c < kRowsB * DP / 4; c += 32) cp_async16(xd + stg_swz<DP>(c), xs + c);
         float *ad = stg + kRowsB * DP;
         if (lane < kRowsB / 4) cp_async16(ad + 4 * lane, p.a + r0 + 4 * lane);
         else if (lane < kRowsB / 2) cp_async16(ad + kRowsB + 4 * (lane - kRowsB / 4), p.u + r0 + 4 * (lane - kRowsB / 4));
@@ -187,7 +187,7 @@ KM_WALK_NAME(AssignParams p)
             const int r = 32 * i + lane;
 #pragma unroll
             for (int j = 0; j < DP; j += 4) {
-                const float4 t = *reinterpret_cast<const float4 *>(stg + r * DP + j);
+                const float4 t = reinterpret_cast<const float4 *>(stg)[stg_swz<DP>(r * (DP / 4) + j / 4)];
                 x[i][j] = t.x; x[i][j + 1] = t.y; x[i][j + 2] = t.z; x[i][j + 3] = t.w;
             }
 #if KM_SKIP1
