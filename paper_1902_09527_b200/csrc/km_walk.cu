@@ -174,6 +174,9 @@ static int walk_threads_rt(int DP) { return walk_threads_of(DP); }
 // DP*4 bytes apart fall on the same banks (DP = 32: an 8-way conflict per quarter warp; ncu of
 // C4: 474M shared bank conflicts, L1 throughput 88 %).  g spreads 8 consecutive rows over the 8
 // 16-byte bank groups.
+#ifndef KM_FLUSH_COORD
+#define KM_FLUSH_COORD 1      // mover deltas: lanes over (mover, coordinate) (0: one lane per mover)
+#endif
 #ifndef KM_SWZ_MIN_DP
 #define KM_SWZ_MIN_DP 16      // DP = 8 rows (32 B) conflict only 2-way; measured separately
 #endif

@@ -144,6 +144,36 @@ KM_WALK_NAME(AssignParams p)
     int mq = 0;
     auto flush_moves = [&]() {
         __syncwarp();
+#if KM_FLUSH_COORD
+        // coordinate-parallel deltas: lanes = (mover, coordinate), 32 / DP movers per step, so
+        // each fp64 RED instruction writes whole row segments of two slab rows (≈ 4x fewer L1
+        // wavefronts / L2 sectors than one lane per mover with 2 (d+1) scattered REDs each)
+        {
+            constexpr int G = DP >= 32 ? 1 : 32 / DP;           // movers per step
+            constexpr int CL = DP >= 32 ? 32 : DP;              // lanes per mover
+            const int nm = min(mq, 32);
+            const int sub = lane / CL, co = lane % CL;
+            for (int m0 = 0; m0 < nm; m0 += G) {
+                const int m = m0 + sub;
+                const bool on = sub < G && m < nm;
+                const int mrow = on ? sQ[m] : 0, mfrom = on ? sQ[kQueue + m] : 0, mto = on ? sQ[2 * kQueue + m] : 0;
+                double *ra = acc + (int64_t)mfrom * (DP + 1), *rb = acc + (int64_t)mto * (DP + 1);
+#pragma unroll
+                for (int j0 = 0; j0 < DP; j0 += CL) {
+                    const int j = j0 + co;
+                    if (on && j < p.d) {
+                        const double v = (double)__ldg(p.X + (size_t)mrow * DP + j);
+                        atomicAdd(rb + j, v);
+                        atomicAdd(ra + j, -v);
+                    }
+                }
+                if (on && co == 0) {
+                    atomicAdd(rb + DP, 1.0);
+                    atomicAdd(ra + DP, -1.0);
+                }
+            }
+        }
+#else
         if (lane < min(mq, 32)) {
             const int mrow = sQ[lane], mfrom = sQ[kQueue + lane], mto = sQ[2 * kQueue + lane];
             float xr[DP];
@@ -155,6 +185,7 @@ KM_WALK_NAME(AssignParams p)
             }
             move_delta<DP>(acc, p.d, mfrom, mto, xr);
         }
+#endif
         __syncwarp();
         if (mq > 32) {   // keep the overflow (< 32 entries) at the front
             int e0 = 0, e1 = 0, e2 = 0;
