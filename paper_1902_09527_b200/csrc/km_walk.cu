@@ -174,6 +174,10 @@ static int walk_threads_rt(int DP) { return walk_threads_of(DP); }
 // DP*4 bytes apart fall on the same banks (DP = 32: an 8-way conflict per quarter warp; ncu of
 // C4: 474M shared bank conflicts, L1 throughput 88 %).  g spreads 8 consecutive rows over the 8
 // 16-byte bank groups.
+#ifndef KM_BULK_MAX_DP
+#define KM_BULK_MAX_DP 0      // rows staged by cp.async.bulk (TMA) up to this width; measured slower at d = 8
+                              // (C3 1.687 vs 1.563 ms per pass: one batch of lookahead hides less latency)
+#endif
 #ifndef KM_FLUSH_COORD
 #define KM_FLUSH_COORD 1      // mover deltas: lanes over (mover, coordinate) (0: one lane per mover)
 #endif
@@ -250,7 +254,8 @@ size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem, bool skip1)
     const int R = DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1);
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
-           (size_t)(walk_threads_rt(DP) / 32) * (32 * R * (DP + 2) + 3 * kQueue + (skip1 ? 64 * R : 0)) * sizeof(float);
+           (size_t)(walk_threads_rt(DP) / 32) *
+               (32 * R * (DP + 2) + 3 * kQueue + (skip1 ? 64 * R : (DP <= KM_BULK_MAX_DP ? 4 : 0))) * sizeof(float);
 }
 
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)

@@ -23,7 +23,12 @@ KM_WALK_NAME(AssignParams p)
     float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2) + 3 * kQueue + 2 * kRowsB);
     float *sAU2 = stg + kRowsB * (DP + 2) + 3 * kQueue;
 #else
-    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2) + 3 * kQueue);
+    // BULK: the batch is staged by the TMA engine (cp.async.bulk, one lane, mbarrier completion)
+    // instead of per-lane cp.async: no LSU wavefronts for the copy (L1 is the busiest unit, ncu)
+    constexpr bool BULK = DP <= KM_BULK_MAX_DP;
+    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2) + 3 * kQueue + (BULK ? 4 : 0));
+    const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(stg + kRowsB * (DP + 2) + 3 * kQueue);
+    uint32_t bphase = 0;
 #endif
     int *sQ = reinterpret_cast<int *>(stg + kRowsB * DP + 2 * kRowsB);   // mover queue: row, from, to
     if (CSMEM) {
@@ -117,6 +122,24 @@ KM_WALK_NAME(AssignParams p)
 #endif
     // stage rows [r0, r0 + 32 R) of X, a, u into this warp's buffer (16-B cp.async per lane)
     auto stage = [&](int r0) {
+#if !KM_SKIP1
+        if constexpr (BULK) {
+            __syncwarp();                           // every lane has read the previous batch
+            if (lane == 0) {
+                const uint32_t xb = kRowsB * DP * 4, ab = kRowsB * 4;
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stg);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sbar), "r"(xb + 2 * ab) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             :: "r"(dst), "l"(p.X + (size_t)r0 * DP), "r"(xb), "r"(sbar) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             :: "r"(dst + xb), "l"(p.a + r0), "r"(ab), "r"(sbar) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             :: "r"(dst + xb + ab), "l"(p.u + r0), "r"(ab), "r"(sbar) : "memory");
+            }
+            return;
+        }
+#endif
         const float4 *xs = reinterpret_cast<const float4 *>(p.X + (size_t)r0 * DP);
         float4 *xd = reinterpret_cast<float4 *>(stg);
 #pragma unroll
@@ -138,6 +161,13 @@ KM_WALK_NAME(AssignParams p)
     asm volatile("cp.async.commit_group;" ::: "memory");
     chunk_row = b0;
 #else
+    if constexpr (BULK) {
+        if (lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sbar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
     if (chunk_row < n) stage(chunk_row);
 #endif
     // mover queue (shared memory, kQueue entries per warp; mq warp-uniform)
@@ -206,7 +236,18 @@ KM_WALK_NAME(AssignParams p)
 #else
         const int row0 = chunk_row + bt * kRows;
 #endif
+#if KM_SKIP1
         asm volatile("cp.async.wait_group 0;" ::: "memory");
+#else
+        if constexpr (BULK) {
+            asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+                         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                         "@!P1 bra WAIT_%=;\n\t}" :: "r"(sbar), "r"(bphase) : "memory");
+            bphase ^= 1u;
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+#endif
         __syncwarp();
         float x[R][DP];
         int aold[R];

@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "c1_free or c2_free or spectral or c5_shaped or B1 or B2 or B5 or dims or ragged or k1 or resum or resort or graph" > gpurun_out/gtest18.log 2>&1; tail -1 gpurun_out/gtest18.log
+bash tools/qv.sh "base nobulk" "c3"
