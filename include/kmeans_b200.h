@@ -59,10 +59,11 @@ enum { KM_PRUNE_MTI = 0, KM_PRUNE_NONE = 1, KM_PRUNE_TI = 2 };
  * whenever the points reassigned since the last sort exceed resort_fraction * n_local. */
 enum { KM_RESORT_AUTO = 0, KM_RESORT_NEVER = 1, KM_RESORT_ALWAYS = 2 };
 
-/* Candidate-evaluation engine of the MTI pass.  AUTO uses the
- * tcgen05 TF32x3 tensor-core kernel when d pads to 8, 16 or 32, else the CUDA-core kernel;
- * both give the same (exact-mode) assignments.  Iteration 1 and KM_PRUNE_NONE always use
- * the CUDA-core dense kernel. */
+/* Candidate-evaluation engine of the MTI pass.  AUTO and CUDA_CORE: the CUDA-core
+ * walk ("k_walk"; "k_walk_skip1" when the previous pass's clause-1 rate exceeds 15 %).  TENSOR:
+ * the tcgen05 TF32x3 kernel ("k_mti_tc"; d padded to 8, 16 or 32; measured slower, opt-in).  All
+ * give the same (exact-mode) assignments.  Iteration 1 and KM_PRUNE_NONE always use the
+ * CUDA-core dense kernel. */
 enum { KM_ENGINE_AUTO = 0, KM_ENGINE_CUDA_CORE = 1, KM_ENGINE_TENSOR = 2 };
 
 typedef struct km_options {
