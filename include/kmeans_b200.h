@@ -113,6 +113,8 @@ typedef struct km_iter_stats {
     float ms_assign;   /* device time of the assignment(+reduction) kernel (this rank) */
     float ms_sort;     /* device time of re-bucketing (0 if none) */
     float ms_comm;     /* device time of the allreduce (0 if world == 1) */
+    int64_t fallbacks; /* rows whose fp32 candidate intervals did not decide the winner and were
+                          re-walked in the direct form (then refined in fp64 if still tied; global) */
 } km_iter_stats;
 
 typedef struct km_ctx km_ctx;
@@ -148,10 +150,22 @@ km_status kmeans_create(int64_t n_local, int32_t d, int32_t k, const float *poin
 km_status kmeans_iterate(km_ctx *ctx, int64_t *changed, int64_t *dists);
 
 /* Iterate until changed <= tol (a count of points; BASELINE uses tol = 0) or max_iters
- * iterations have run in this call.  max_iters = 0 runs nothing (iterations = 0, centroids
- * unchanged).  iterations / dists_total (may be NULL) receive this call's totals. */
+ * iterations have run in this call, then kmeans_finalize.  max_iters = 0 runs nothing
+ * (iterations = 0, centroids unchanged).  iterations / dists_total (may be NULL) receive this
+ * call's totals. */
 km_status kmeans_run(km_ctx *ctx, int32_t max_iters, int64_t tol, int32_t *iterations,
                      int64_t *dists_total);
+
+/* Re-derive C_T = per-cluster means of a_T from sums taken in one fixed order (DESIGN.md
+ * reading B12; Lloyd's update): each rank sums its rows in its own row
+ * order in blocks of 65536 rows (per block and cluster a sequential fp64 sum from 0, then the
+ * block sums added from 0 in block order), then the ranks' sums are added.  The iterations keep
+ * running sums updated by the moves of each pass (reading B5), whose fp64 rounding depends on
+ * the order the moves are applied in; after finalize the centroids are bit-reproducible run to
+ * run for the same assignments (world <= 2: independent of NCCL's reduction order).  The
+ * centroids of the last pass are kept for the next drift, so iterating further stays sound.
+ * Collective when world > 1.  No-op before iteration 1.  kmeans_run calls it. */
+km_status kmeans_finalize(km_ctx *ctx);
 
 /* n_local int32 assignments of the last assignment pass, in the caller's row order
  * (reading A9: not re-argmin against the final centroids).  out is host memory unless

@@ -35,7 +35,7 @@ class KmIterStats(ct.Structure):
     _fields_ = [("changed", ct.c_int64), ("dists", ct.c_int64), ("clause1", ct.c_int64),
                 ("refined", ct.c_int64), ("walk_steps", ct.c_int64), ("empty", ct.c_int32), ("resorted", ct.c_int32),
                 ("ms_iter", ct.c_float), ("ms_assign", ct.c_float), ("ms_sort", ct.c_float),
-                ("ms_comm", ct.c_float)]
+                ("ms_comm", ct.c_float), ("fallbacks", ct.c_int64)]
 
 
 # name -> (restype, argtypes); the list is also the export check of tests/test_capi_symbols.py
@@ -45,6 +45,7 @@ SIGNATURES = {
     "kmeans_create": (ct.c_int32, [ct.c_int64, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_void_p,
                                    ct.POINTER(KmOptions), ct.POINTER(ct.c_void_p)]),
     "kmeans_iterate": (ct.c_int32, [ct.c_void_p, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]),
+    "kmeans_finalize": (ct.c_int32, [ct.c_void_p]),
     "kmeans_run": (ct.c_int32, [ct.c_void_p, ct.c_int32, ct.c_int64, ct.POINTER(ct.c_int32),
                                 ct.POINTER(ct.c_int64)]),
     "kmeans_get_assignments": (ct.c_int32, [ct.c_void_p, ct.c_void_p, ct.c_int32]),

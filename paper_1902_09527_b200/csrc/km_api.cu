@@ -171,6 +171,7 @@ struct km_ctx {
     unsigned *eps_bits = nullptr;
     double *sse_buf = nullptr;
     int32_t *a_out = nullptr;
+    double *exact_P = nullptr;      // exact-order sums: per 64 Ki-row block x cluster partials (B12)
     HostStat *hstat = nullptr;
     int grid_assign[4] = {0, 0, 0, 0};
     float g_up = 1.f, g_dn = 1.f;
@@ -327,6 +328,19 @@ km_status resort(km_ctx *c)
     return KM_OK;
 }
 
+// c->acc = this rank's per-cluster sums | counts of the current assignment in the exact order of
+// reading B12 (caller row order, 64 Ki-row blocks merged in block order): bit-reproducible.
+// Scratch: keys (inverse permutation), the idle row buffer's a (caller-order assignments).
+km_status exact_sums(km_ctx *c)
+{
+    int l = 0;
+    KM_CUDA(km::launch_exact_sums(c->X[c->cur], c->a[c->cur], c->perm[c->cur], c->n, c->DP, c->k,
+                                  reinterpret_cast<int32_t *>(c->keys), c->a[1 - c->cur], c->exact_P, c->acc,
+                                  c->st, &l));
+    c->launches += l;
+    return KM_OK;
+}
+
 km_status allreduce(km_ctx *c)
 {
     if (!c->comm_on) return KM_OK;   // global counters = local (iterate copies them once)
@@ -372,10 +386,7 @@ km_status enqueue_body(km_ctx *c, bool full = false)
     KM_CUDA(rec_event(ev[2], c->st));
     KM_TRY(launch_assign(c, c->prune != KM_PRUNE_NONE ? km::MODE_MTI_REDUCE : km::MODE_DENSE_REDUCE, 0));
     KM_CUDA(rec_event(ev[3], c->st));
-    if (full) {
-        KM_CUDA(cudaMemsetAsync(c->acc_part, 0, (size_t)c->nslab * c->k * (c->DP + 1) * sizeof(double), c->st));
-        KM_TRY(launch_assign(c, km::MODE_REDUCE_ONLY, 1));
-    }
+    if (full) KM_TRY(exact_sums(c));   // re-derive the sums from every row (exact order, B12)
     KM_CUDA(rec_event(ev[4], c->st));
     KM_TRY(allreduce(c));
     KM_CUDA(rec_event(ev[5], c->st));
@@ -455,7 +466,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
             KM_TRY(resort(c));
             sorted_now = true;
         }
-        KM_TRY(launch_assign(c, km::MODE_REDUCE_ONLY, 1));
+        KM_TRY(exact_sums(c));
         KM_CUDA(cudaEventRecord(ev[4], c->st));
         KM_TRY(allreduce(c));
         KM_CUDA(cudaEventRecord(ev[5], c->st));
@@ -498,6 +509,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
     c->skip1 = (double)rec.clause1 > kSkip1Rate * (double)c->n_global;
     rec.refined = (int64_t)h->global[3];
     rec.walk_steps = (int64_t)h->global[4];
+    rec.fallbacks = (int64_t)h->global[5];
     rec.empty = h->empty;
     rec.resorted = sorted_now;
     rec.ms_assign = elapsed(ev[2], ev[3]);
@@ -517,7 +529,7 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base); cudaFree(c->lohist); cudaFree(c->qmap);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out);
+    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P);
     cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part); cudaFree(c->L); cudaFree(c->Hm);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -584,6 +596,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     const int NBmax = k * c->Q;
     c->ntiles = (int)((n + c->tile_rows - 1) / c->tile_rows);
     KM_TRY(dalloc(&c->keys, (size_t)n));
+    KM_TRY(dalloc(&c->exact_P, (size_t)km::exact_blocks(n) * k * (DP + 1)));
     KM_TRY(dalloc(&c->hist, (size_t)NBmax * c->ntiles));
     KM_TRY(dalloc(&c->totals, (size_t)NBmax));
     KM_TRY(dalloc(&c->lohist, (size_t)k + 1));
@@ -808,6 +821,30 @@ km_status kmeans_iterate(km_ctx *c, int64_t *changed, int64_t *dists)
     return iterate(c, changed, dists);
 }
 
+// C_T re-derived from exact-order sums of a_T (reading B12); C_prev (the centroids of the last
+// pass) is kept, so iterating further stays sound.  No-op before the first iteration.
+km_status finalize(km_ctx *c)
+{
+    KM_CUDA(cudaSetDevice(c->device));
+    if (c->t == 0) return KM_OK;
+    KM_CUDA(cudaMemsetAsync(c->scratch, 0, c->scratch_bytes, c->st));
+    KM_TRY(exact_sums(c));
+    KM_TRY(allreduce(c));
+    KM_CUDA(km::launch_update(c->acc, c->S, 2, c->C, c->Cprev, c->k, c->d, c->DP, c->empty,
+                              c->spherical ? 1 : 0, c->st));
+    c->launches += 1;
+    KM_CUDA(cudaStreamSynchronize(c->st));
+    c->moves_since_full = 0;
+    return KM_OK;
+}
+
+km_status kmeans_finalize(km_ctx *c)
+{
+    g_err.clear();
+    if (!c) return fail(KM_EARG, "ctx is NULL");
+    return finalize(c);
+}
+
 km_status kmeans_run(km_ctx *c, int32_t max_iters, int64_t tol, int32_t *iterations, int64_t *dists_total)
 {
     g_err.clear();
@@ -823,6 +860,7 @@ km_status kmeans_run(km_ctx *c, int32_t max_iters, int64_t tol, int32_t *iterati
         tot += ds;
         if (ch <= tol) break;
     }
+    if (it > 0) KM_TRY(finalize(c));
     if (iterations) *iterations = it;
     if (dists_total) *dists_total = tot;
     return KM_OK;

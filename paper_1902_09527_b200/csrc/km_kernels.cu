@@ -394,7 +394,9 @@ cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems,
 // ---------------------------------------------------------------------------------------
 // S4: C_new[c] = sums[c] / count[c] (IEEE fp64 division), or C_old[c] when empty (A10).
 // S holds the running per-cluster sums | count: delta = 0 -> S = acc (full reduction of this
-// pass), delta = 1 -> S += acc (acc holds only the moves of this pass).
+// pass), delta = 1 -> S += acc (acc holds only the moves of this pass),
+// delta = 2 -> S = acc with C_prev kept (kmeans_finalize: C_T re-derived from exact-order sums of
+// the same assignment; C_prev stays the centroids the last pass used, so the drift stays sound).
 __global__ void k_update(const double *acc, double *S, int delta, double *C, double *Cprev, int k, int d,
                          int DP, int *empty, int spherical)
 {
@@ -402,15 +404,16 @@ __global__ void k_update(const double *acc, double *S, int delta, double *C, dou
     if (c >= k) return;
     double *Sc = S + (int64_t)c * (DP + 1);
     const double *ac = acc + (int64_t)c * (DP + 1);
-    const double cnt = delta ? Sc[DP] + ac[DP] : ac[DP];
+    const bool add = delta == 1, keep_prev = delta == 2;
+    const double cnt = add ? Sc[DP] + ac[DP] : ac[DP];
     Sc[DP] = cnt;
     if (!(cnt > 0.5)) atomicAdd(empty, 1);
     for (int j = 0; j < d; ++j) {
-        const double v = delta ? Sc[j] + ac[j] : ac[j];
+        const double v = add ? Sc[j] + ac[j] : ac[j];
         Sc[j] = v;
         const int64_t ci = (int64_t)c * d + j;
         const double old = C[ci];
-        Cprev[ci] = old;
+        if (!keep_prev) Cprev[ci] = old;
         C[ci] = cnt > 0.5 ? v / cnt : old;
     }
     if (spherical && cnt > 0.5) {
@@ -433,6 +436,99 @@ cudaError_t launch_update(const double *acc, double *S, int delta, double *C, do
                           int DP, int *empty, int spherical, cudaStream_t st)
 {
     k_update<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(acc, S, delta, C, Cprev, k, d, DP, empty, spherical);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Exact-order cluster sums (reading B12).  The rows are summed in the caller's row
+// order, in blocks of kExactBlock rows: per block and cluster a sequential fp64 sum from 0 over
+// the block's rows of that cluster in row order, then per cluster the block sums added from 0 in
+// block order — one fixed order, independent of the physical (re-bucketed) row order, of the
+// grid and of timing, so C_T is bit-reproducible run to run (and, being the order the oracle's
+// reduction is defined with, bit-identical to the oracle's when the assignments agree).
+__global__ void k_unpermute(const int32_t *a, const int32_t *perm, int64_t n, int32_t *out);
+constexpr int kExactThreads = 128;     // clusters per CTA
+constexpr int kExactTile = 4096;       // assignments staged in shared memory per step
+
+__global__ void k_inv_perm(const int32_t *perm, int64_t n, int32_t *inv)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        inv[perm[i]] = (int32_t)i;
+}
+
+// CTA (block b, clusters [128 y, 128 y + 128)): every thread scans the block's caller-order
+// assignments (broadcast from shared memory) and adds the rows of its own cluster in row order.
+template <int DP>
+__global__ void __launch_bounds__(kExactThreads) k_exact_block_sums(const float *X, const int32_t *inv,
+                                                                   const int32_t *ac, int64_t n, int k,
+                                                                   double *P)
+{
+    __shared__ __align__(16) int32_t sa[kExactTile];
+    const int64_t r0 = (int64_t)blockIdx.x * kExactBlock;
+    const int64_t r1 = r0 + kExactBlock < n ? r0 + kExactBlock : n;
+    const int c = blockIdx.y * kExactThreads + threadIdx.x;
+    double s[DP];
+#pragma unroll
+    for (int j = 0; j < DP; ++j) s[j] = 0.0;
+    double cnt = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += kExactTile) {
+        const int m = (int)(r1 - t0 < kExactTile ? r1 - t0 : kExactTile);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += kExactThreads) sa[i] = ac[t0 + i];
+        __syncthreads();
+        for (int i = 0; i < m; ++i) {
+            if (sa[i] != c) continue;
+            const float4 *xr = reinterpret_cast<const float4 *>(X + (int64_t)inv[t0 + i] * DP);
+#pragma unroll
+            for (int j = 0; j < DP / 4; ++j) {
+                const float4 v = __ldg(xr + j);
+                s[4 * j] = __dadd_rn(s[4 * j], (double)v.x);
+                s[4 * j + 1] = __dadd_rn(s[4 * j + 1], (double)v.y);
+                s[4 * j + 2] = __dadd_rn(s[4 * j + 2], (double)v.z);
+                s[4 * j + 3] = __dadd_rn(s[4 * j + 3], (double)v.w);
+            }
+            cnt += 1.0;
+        }
+    }
+    if (c < k) {
+        double *pb = P + ((int64_t)blockIdx.x * k + c) * (DP + 1);
+#pragma unroll
+        for (int j = 0; j < DP; ++j) pb[j] = s[j];
+        pb[DP] = cnt;
+    }
+}
+
+// acc[c][j] = ((0 + P_0[c][j]) + P_1[c][j]) + ... in block order
+__global__ void k_exact_merge(const double *P, int64_t nblk, int64_t elems, double *acc)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= elems) return;
+    double s = 0.0;
+    for (int64_t b = 0; b < nblk; ++b) s = __dadd_rn(s, P[b * elems + t]);
+    acc[t] = s;
+}
+
+int64_t exact_blocks(int64_t n) { return (n + kExactBlock - 1) / kExactBlock; }
+
+cudaError_t launch_exact_sums(const float *X, const int32_t *a, const int32_t *perm, int64_t n, int DP, int k,
+                              int32_t *inv, int32_t *ac, double *P, double *acc, cudaStream_t st, int *launches)
+{
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    k_inv_perm<<<g, 256, 0, st>>>(perm, n, inv);
+    k_unpermute<<<g, 256, 0, st>>>(a, perm, n, ac);
+    const int64_t nblk = exact_blocks(n);
+    const dim3 grid((unsigned)nblk, (unsigned)((k + kExactThreads - 1) / kExactThreads));
+    switch (DP) {
+    case 4: k_exact_block_sums<4><<<grid, kExactThreads, 0, st>>>(X, inv, ac, n, k, P); break;
+    case 8: k_exact_block_sums<8><<<grid, kExactThreads, 0, st>>>(X, inv, ac, n, k, P); break;
+    case 16: k_exact_block_sums<16><<<grid, kExactThreads, 0, st>>>(X, inv, ac, n, k, P); break;
+    case 32: k_exact_block_sums<32><<<grid, kExactThreads, 0, st>>>(X, inv, ac, n, k, P); break;
+    case 64: k_exact_block_sums<64><<<grid, kExactThreads, 0, st>>>(X, inv, ac, n, k, P); break;
+    default: return cudaErrorInvalidValue;
+    }
+    const int64_t elems = (int64_t)k * (DP + 1);
+    k_exact_merge<<<(unsigned)((elems + 255) / 256), 256, 0, st>>>(P, nblk, elems, acc);
+    *launches += 4;
     return cudaGetLastError();
 }
 

@@ -96,7 +96,8 @@ struct SortParams {
     int32_t ks;
     int32_t k, DP, Q, NB, ntiles, tile_rows;
 };
-constexpr int kQuantK = 8192;   // quantile prefix classes for k <= this (p packed in 13 bits)
+constexpr int kQuantK = 8192;
+constexpr int64_t kExactBlock = 65536;   // rows per block of the exact-order sums (reading B12)   // quantile prefix classes for k <= this (p packed in 13 bits)
 
 // ---- launchers (km_kernels.cu) ----------------------------------------------------------
 cudaError_t launch_prep(const PrepParams &p, cudaStream_t st);
@@ -130,6 +131,9 @@ cudaError_t launch_update(const double *acc, double *S, int delta, double *C, do
 cudaError_t launch_sort(const SortParams &p, cudaStream_t st, int *launches);
 cudaError_t launch_sse(const float *X, const int32_t *a, const double *C, int64_t n, int d,
                        int DP, double *out, cudaStream_t st);
+int64_t exact_blocks(int64_t n);
+cudaError_t launch_exact_sums(const float *X, const int32_t *a, const int32_t *perm, int64_t n, int DP, int k,
+                              int32_t *inv, int32_t *ac, double *P, double *acc, cudaStream_t st, int *launches);
 cudaError_t launch_unpermute(const int32_t *a, const int32_t *perm, int64_t n, int32_t *out,
                              cudaStream_t st);
 cudaError_t launch_iota(int32_t *perm, int64_t n, cudaStream_t st);

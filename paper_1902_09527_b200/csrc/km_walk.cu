@@ -51,6 +51,13 @@ namespace km {
 constexpr int kWalkChunk = KM_WALK_CHUNK;   // rows a warp claims per work-counter fetch
 constexpr int kQueue = 64;             // mover-queue entries per warp (< 32 left + 32 new)
 
+// floats of one warp's shared-memory region: staged rows x | a | u, mover queue (row, from, to)
+// [, SKIP1: the second a | u slot]
+__host__ __device__ constexpr int walk_warp_floats(int DP, int R, int skip1)
+{
+    return 32 * R * (DP + 2) + 3 * kQueue + (skip1 ? 64 * R : 0);
+}
+
 __host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // float4 per candidate pair
 
 // 32-byte read-only load (LDG.E.ENL2.256): two float4 in one instruction
@@ -84,8 +91,9 @@ __device__ __forceinline__ float2 add2s(float a, float2 b)
 }
 
 // squared distances to the candidate pair (j, j+1) in the centred expansion form:
-// (q_j, q_j+1) = (xx + cc_j, xx + cc_j+1) + sum_e x'_e (m_j[e], m_j+1[e]),  m = -2 c'
-// v: the pair's DP/2 float4 (coordinates interleaved by candidate); one FFMA2 per coordinate
+// (q_j, q_j+1) = (xx + cc_j, xx + cc_j+1) + sum_e x'_e (m_j[e], m_j+1[e]),  m = -2 c', cc = |c'|^2
+// v: the pair's DP/2 float4 (coordinates interleaved by candidate); one FFMA2 (scalar x'_e
+// broadcast) per coordinate
 template <int DP>
 __device__ __forceinline__ float2 q_pair(const float (&xc)[DP], float xx, float2 cc, const float4 (&v)[DP / 2])
 {
@@ -174,15 +182,9 @@ static int walk_threads_rt(int DP) { return walk_threads_of(DP); }
 // DP*4 bytes apart fall on the same banks (DP = 32: an 8-way conflict per quarter warp; ncu of
 // C4: 474M shared bank conflicts, L1 throughput 88 %).  g spreads 8 consecutive rows over the 8
 // 16-byte bank groups.
-#ifndef KM_BULK_MAX_DP
-#define KM_BULK_MAX_DP 0      // rows staged by cp.async.bulk (TMA) up to this width; measured slower at d = 8
-                              // (C3 1.687 vs 1.563 ms per pass: one batch of lookahead hides less latency)
-#endif
-#ifndef KM_FLUSH_COORD
-#define KM_FLUSH_COORD 1      // mover deltas: lanes over (mover, coordinate) (0: one lane per mover)
-#endif
 #ifndef KM_SWZ_MIN_DP
-#define KM_SWZ_MIN_DP 16      // DP = 8 rows (32 B) conflict only 2-way; measured separately
+#define KM_SWZ_MIN_DP 8       // DP = 8: unswizzled 32-B rows read 2-way conflicted (ncu of C3: the
+                              // staging writes and reads were 57 % of the shared wavefronts)
 #endif
 template <int DP>
 __device__ __forceinline__ int stg_swz(int c)
@@ -254,8 +256,7 @@ size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem, bool skip1)
     const int R = DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1);
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
-           (size_t)(walk_threads_rt(DP) / 32) *
-               (32 * R * (DP + 2) + 3 * kQueue + (skip1 ? 64 * R : (DP <= KM_BULK_MAX_DP ? 4 : 0))) * sizeof(float);
+           (size_t)(walk_threads_rt(DP) / 32) * walk_warp_floats(DP, R, skip1 ? 1 : 0) * sizeof(float);
 }
 
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)

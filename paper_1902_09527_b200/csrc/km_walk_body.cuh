@@ -18,17 +18,10 @@ KM_WALK_NAME(AssignParams p)
     float *sH = sS + k4;                            // k x NH H rows (HSMEM)
     // per-warp staging of the next batch (cp.async): x rows, then a, then u
     constexpr int kRowsB = 32 * R;
+    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * walk_warp_floats(DP, R, KM_SKIP1);
 #if KM_SKIP1
     // a second [a | u] slot: the a/u of the batch after the one whose rows are staged
-    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2) + 3 * kQueue + 2 * kRowsB);
     float *sAU2 = stg + kRowsB * (DP + 2) + 3 * kQueue;
-#else
-    // BULK: the batch is staged by the TMA engine (cp.async.bulk, one lane, mbarrier completion)
-    // instead of per-lane cp.async: no LSU wavefronts for the copy (L1 is the busiest unit, ncu)
-    constexpr bool BULK = DP <= KM_BULK_MAX_DP;
-    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * (kRowsB * (DP + 2) + 3 * kQueue + (BULK ? 4 : 0));
-    const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(stg + kRowsB * (DP + 2) + 3 * kQueue);
-    uint32_t bphase = 0;
 #endif
     int *sQ = reinterpret_cast<int *>(stg + kRowsB * DP + 2 * kRowsB);   // mover queue: row, from, to
     if (CSMEM) {
@@ -66,7 +59,6 @@ KM_WALK_NAME(AssignParams p)
     unsigned long long c_dists = 0;
     unsigned c_changed32 = 0, c_clause132 = 0, c_refined32 = 0, c_fb32 = 0, steps32 = 0;
 
-    constexpr int kBatches = kWalkChunk / kRows;
     auto claim = [&]() -> int {
         int c = 0;
         if (lane == 0) c = atomicAdd(p.work, 1);
@@ -117,29 +109,17 @@ KM_WALK_NAME(AssignParams p)
     };
     int chunk_row = n;
 #else
-    int chunk_row = claim(), ahead_row = claim();
+    // the work counter is fetched one chunk ahead by lane 0 and broadcast only when that chunk
+    // starts, so the atomic's round trip overlaps a whole chunk of work
+    constexpr int kBatches = kWalkChunk / kRows;
+    const int nchunks = (n + kWalkChunk - 1) / kWalkChunk;
+    int chunk_row = claim();
+    int ahead_c = 0;                                // lane 0: the claimed chunk after chunk_row
+    if (lane == 0) ahead_c = atomicAdd(p.work, 1);
     int bt = 0;
 #endif
     // stage rows [r0, r0 + 32 R) of X, a, u into this warp's buffer (16-B cp.async per lane)
     auto stage = [&](int r0) {
-#if !KM_SKIP1
-        if constexpr (BULK) {
-            __syncwarp();                           // every lane has read the previous batch
-            if (lane == 0) {
-                const uint32_t xb = kRowsB * DP * 4, ab = kRowsB * 4;
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stg);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sbar), "r"(xb + 2 * ab) : "memory");
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             :: "r"(dst), "l"(p.X + (size_t)r0 * DP), "r"(xb), "r"(sbar) : "memory");
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             :: "r"(dst + xb), "l"(p.a + r0), "r"(ab), "r"(sbar) : "memory");
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             :: "r"(dst + xb + ab), "l"(p.u + r0), "r"(ab), "r"(sbar) : "memory");
-            }
-            return;
-        }
-#endif
         const float4 *xs = reinterpret_cast<const float4 *>(p.X + (size_t)r0 * DP);
         float4 *xd = reinterpret_cast<float4 *>(stg);
 #pragma unroll
@@ -161,40 +141,46 @@ KM_WALK_NAME(AssignParams p)
     asm volatile("cp.async.commit_group;" ::: "memory");
     chunk_row = b0;
 #else
-    if constexpr (BULK) {
-        if (lane == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sbar) : "memory");
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncwarp();
-    }
     if (chunk_row < n) stage(chunk_row);
 #endif
     // mover queue (shared memory, kQueue entries per warp; mq warp-uniform)
     int mq = 0;
     auto flush_moves = [&]() {
         __syncwarp();
-#if KM_FLUSH_COORD
         // coordinate-parallel deltas: lanes = (mover, coordinate), 32 / DP movers per step, so
-        // each fp64 RED instruction writes whole row segments of two slab rows (≈ 4x fewer L1
-        // wavefronts / L2 sectors than one lane per mover with 2 (d+1) scattered REDs each)
+        // each fp64 RED instruction writes whole row segments of two slab rows; all the movers'
+        // coordinates are loaded before the first RED (one L2 round trip per flush, not per step)
         {
             constexpr int G = DP >= 32 ? 1 : 32 / DP;           // movers per step
             constexpr int CL = DP >= 32 ? 32 : DP;              // lanes per mover
+            constexpr int NS = 32 / G;                          // steps for 32 movers
+            constexpr int NJ = DP >= 32 ? DP / 32 : 1;          // coordinates per lane per step
             const int nm = min(mq, 32);
             const int sub = lane / CL, co = lane % CL;
-            for (int m0 = 0; m0 < nm; m0 += G) {
-                const int m = m0 + sub;
-                const bool on = sub < G && m < nm;
-                const int mrow = on ? sQ[m] : 0, mfrom = on ? sQ[kQueue + m] : 0, mto = on ? sQ[2 * kQueue + m] : 0;
+            float xv[NS][NJ];
+#pragma unroll
+            for (int st = 0; st < NS; ++st) {
+                const int m = st * G + sub;
+                const int mrow = m < nm ? sQ[m] : -1;
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj) {
+                    const int j = jj * CL + co;
+                    xv[st][jj] = (mrow >= 0 && j < p.d) ? __ldg(p.X + (size_t)mrow * DP + j) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int st = 0; st < NS; ++st) {
+                const int m = st * G + sub;
+                if (st * G >= nm) break;
+                const bool on = m < nm;
+                const int mfrom = on ? sQ[kQueue + m] : 0, mto = on ? sQ[2 * kQueue + m] : 0;
                 double *ra = acc + (int64_t)mfrom * (DP + 1), *rb = acc + (int64_t)mto * (DP + 1);
 #pragma unroll
-                for (int j0 = 0; j0 < DP; j0 += CL) {
-                    const int j = j0 + co;
+                for (int jj = 0; jj < NJ; ++jj) {
+                    const int j = jj * CL + co;
                     if (on && j < p.d) {
-                        const double v = (double)__ldg(p.X + (size_t)mrow * DP + j);
-                        atomicAdd(rb + j, v);
-                        atomicAdd(ra + j, -v);
+                        atomicAdd(rb + j, (double)xv[st][jj]);
+                        atomicAdd(ra + j, -(double)xv[st][jj]);
                     }
                 }
                 if (on && co == 0) {
@@ -203,19 +189,6 @@ KM_WALK_NAME(AssignParams p)
                 }
             }
         }
-#else
-        if (lane < min(mq, 32)) {
-            const int mrow = sQ[lane], mfrom = sQ[kQueue + lane], mto = sQ[2 * kQueue + lane];
-            float xr[DP];
-            const float4 *src = reinterpret_cast<const float4 *>(p.X + (size_t)mrow * DP);
-#pragma unroll
-            for (int j = 0; j < DP / 4; ++j) {
-                const float4 t = __ldg(src + j);
-                xr[4 * j] = t.x; xr[4 * j + 1] = t.y; xr[4 * j + 2] = t.z; xr[4 * j + 3] = t.w;
-            }
-            move_delta<DP>(acc, p.d, mfrom, mto, xr);
-        }
-#endif
         __syncwarp();
         if (mq > 32) {   // keep the overflow (< 32 entries) at the front
             int e0 = 0, e1 = 0, e2 = 0;
@@ -236,18 +209,7 @@ KM_WALK_NAME(AssignParams p)
 #else
         const int row0 = chunk_row + bt * kRows;
 #endif
-#if KM_SKIP1
         asm volatile("cp.async.wait_group 0;" ::: "memory");
-#else
-        if constexpr (BULK) {
-            asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-                         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-                         "@!P1 bra WAIT_%=;\n\t}" :: "r"(sbar), "r"(bphase) : "memory");
-            bphase ^= 1u;
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-#endif
         __syncwarp();
         float x[R][DP];
         int aold[R];
@@ -293,8 +255,9 @@ KM_WALK_NAME(AssignParams p)
 #else
         if (++bt == kBatches || chunk_row + bt * kRows >= n) {
             bt = 0;
-            chunk_row = ahead_row;
-            ahead_row = chunk_row < n ? claim() : ahead_row;
+            const int c = __shfl_sync(kFull, ahead_c, 0);
+            chunk_row = c < nchunks ? c * kWalkChunk : n;
+            if (lane == 0 && chunk_row < n) ahead_c = atomicAdd(p.work, 1);
         }
         if (chunk_row < n) stage(chunk_row + bt * kRows);
 #endif
@@ -358,6 +321,9 @@ KM_WALK_NAME(AssignParams p)
             // the walk: candidates j < pm of A's list, two per step, keys (q & kmask) | j
             const float4 *blk = p.Wblk + (int64_t)A * (kp / 2) * walk_pair_f4(DP);
             const float2 *ccA = reinterpret_cast<const float2 *>(p.Wcc + (int64_t)A * kp);
+            // prefix max of |c'|^2 over the rows the walk evaluates (bounds the error of every
+            // key); loaded before the walk so its latency overlaps it
+            const float cmax = pm > 0 ? __ldg(p.Wmeta + (int64_t)A * kp + ((pm + 1) & ~1) - 1).x : 0.f;
             int m1[R], m2[R];
 #pragma unroll
             for (int i = 0; i < R; ++i) { m1[i] = 0x7fffffff; m2[i] = 0x7fffffff; }
@@ -385,14 +351,9 @@ KM_WALK_NAME(AssignParams p)
                     }
                 } else {
                     float4 v[DP / 2];
-                    if constexpr (DP >= 32) {   // halves the load instructions where they dominate
 #pragma unroll
-                        for (int e = 0; e < DP / 2; e += 2)
-                            ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e, v[e], v[e + 1]);
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < DP / 2; ++e) v[e] = __ldg(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e);
-                    }
+                    for (int e = 0; e < DP / 2; e += 2)      // 32-byte loads: half the L1 requests
+                        ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e, v[e], v[e + 1]);
 #pragma unroll
                     for (int i = 0; i < R; ++i) q[i] = q_pair<DP>(xc[i], xx[i], cc, v);
                 }
@@ -407,8 +368,6 @@ KM_WALK_NAME(AssignParams p)
                 }
             }
             steps32 += (unsigned)pm;
-            // prefix max of |c'|^2 over the evaluated rows (bounds the error of every key)
-            const float cmax = pm > 0 ? __ldg(p.Wmeta + (int64_t)A * kp + ((pm + 1) & ~1) - 1).x : 0.f;
             const float2 *mA = p.Wmeta + (int64_t)A * kp;
 #pragma unroll
             for (int i = 0; i < R; ++i) {
@@ -534,7 +493,7 @@ KM_WALK_NAME(AssignParams p)
                 if (lane == 0 && rb < n) p.dcount[rb / 32] = __popc(dm);
             }
             if (valid[i]) {
-                p.a[rb + lane] = anew[i];
+                if (anew[i] != aold[i]) p.a[rb + lane] = anew[i];
                 p.u[rb + lane] = unew[i];
             }
             // S3 as a delta (B5): movers are queued in shared memory and their fp64

@@ -96,6 +96,11 @@ class KMeans:
         C.check(C.lib().kmeans_iterate(self._h, ct.byref(ch), ct.byref(ds)))
         return ch.value, ds.value
 
+    def finalize(self):
+        """C_T re-derived from exact-order sums of the current assignment (``kmeans_finalize``,
+        DESIGN.md reading B12): bit-reproducible centroids.  ``run`` calls it."""
+        C.check(C.lib().kmeans_finalize(self._h))
+
     def run(self, max_iters: int, tol: int = 0):
         it, ds = ct.c_int32(), ct.c_int64()
         C.check(C.lib().kmeans_run(self._h, int(max_iters), int(tol), ct.byref(it), ct.byref(ds)))

@@ -44,7 +44,7 @@ def test_library_is_sm100a():
 def test_struct_layouts():
     from paper_1902_09527_b200 import _capi
     assert ct.sizeof(_capi.KmOptions) == 216
-    assert ct.sizeof(_capi.KmIterStats) == 64
+    assert ct.sizeof(_capi.KmIterStats) == 72
     o = _capi.KmOptions()
     _capi.lib().kmeans_default_options(ct.byref(o))
     assert o.world == 1 and o.prune == 0 and o.resort_fraction == 0.0 and o.engine == 0

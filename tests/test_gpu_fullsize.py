@@ -92,4 +92,8 @@ def test_full_size_trajectory(name):
     assert t == T
     assert np.array_equal(a[::g["sample_stride"]], asamp)
     assert abs(km.sse() - g["final_sse"]) <= 1e-12 * g["final_sse"]
+    # exact-order sums of a_T (reading B12) reproduce the oracle's C_T bit for bit
+    km.finalize()
+    assert np.array_equal(km.centroids(), Cg[T - 1]), float(np.abs(km.centroids() - Cg[T - 1]).max())
+    assert abs(km.sse() - g["final_sse"]) <= 1e-12 * g["final_sse"]
     km.close()
