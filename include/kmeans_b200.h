@@ -198,8 +198,8 @@ km_status kmeans_get_stats(km_ctx *ctx, km_iter_stats *out, int32_t cap, int32_t
  * points_on_host = 1 (copied).  c_1 = row first_index; c_m (m = 2..k) = the row drawn with
  * probability D(x)^2 / sum D^2 using the caller's uniforms[m-2] in [0,1) (k-1 values, host).
  * The draw is exact and reproducible (reading B9): D^2 in fp64 summed in coordinate
- * order; sum D^2 hierarchically (1024-row blocks, 1024-block groups, each level in order);
- * u * sum located top-down by the running sums of each level.  Outputs (host, caller-owned): chosen[k] row indices, centroids k x d fp64 (the
+ * order; the drawn row is the first row whose exact prefix sum of D^2 exceeds u times the exact
+ * total (the sums are kept as 768-bit fixed-point integers, exact for any fp32 data).  Outputs (host, caller-owned): chosen[k] row indices, centroids k x d fp64 (the
  * chosen rows).  Errors: KM_EARG (sizes, NULLs, first_index out of range, uniforms outside
  * [0,1), fewer than k distinct rows), KM_ECUDA, KM_ENOMEM.  stream: cudaStream_t or NULL. */
 km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *points, int32_t points_on_host,

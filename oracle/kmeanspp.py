@@ -1,20 +1,28 @@
-"""k-means++ D² seeding oracle — TEST INFRASTRUCTURE ONLY.
+"""k-means++ D² seeding oracle — TEST INFRASTRUCTURE ONLY (only tests/, smoke() and bench.py's
+cpu_baseline may import it; the product path never does).
 
 PAPER.md §4.3 "k-means++" (lines 1141-1159), Eq. 2: each new centroid is drawn from the data
 with probability D(v)² / Σ_v D(v)², D(v) = the distance of v to the nearest centroid already
-chosen.  Reading B9 makes the draw reproducible and exact: the caller supplies
-the first index and the k-1 uniforms; D² is summed in fp64 over the coordinates in order; the
-total is formed over fixed blocks of 65536 rows (each summed in row order, the block sums added
-in block order); the chosen row is the first row of the first block whose running block sum
-exceeds u·total, whose in-block running sum exceeds u·total minus the preceding blocks' sum,
-and whose D² is positive.  Written as plain loops: slow, obviously in order.
+chosen.  Reading B9 makes the draw reproducible and exact:
+
+* the caller supplies the first index and the k-1 uniforms u ∈ [0, 1);
+* D(v)² is the fp64 value Σ_j (x_j - c_j)² computed in coordinate order (each difference,
+  square and addition rounded to nearest), minimised over the chosen centres;
+* the drawn row is the FIRST row i whose exact prefix sum Σ_{j<=i} D_j² exceeds u · Σ_j D_j²,
+  prefix, total and product taken exactly (real arithmetic on the fp64 values).
+
+The exact sums are Python integers: every D² is a multiple of 2^-350 (differences of fp32
+values are multiples of 2^-149, so their squares and the rounded sums of squares are multiples
+of 2^-298 rounded to 53 bits), so D² · 2^350 is an exact integer.  Written as plain loops over
+the rows: slow, obviously the definition.  Nothing here mirrors the GPU's blocking.
 """
 from __future__ import annotations
 
+from itertools import accumulate
+
 import numpy as np
 
-BLOCK = 1024        # rows per block
-GROUP = 1024        # blocks per group
+SCALE_BITS = 350           # D² * 2^SCALE_BITS is an integer for every D² (see above)
 
 
 def d2_to(X64, c):
@@ -26,64 +34,30 @@ def d2_to(X64, c):
     return s
 
 
-def _seq_sum(vals):
-    """Left-to-right sum (np.add.accumulate is a sequential loop); 0.0 for an empty list."""
-    return float(np.add.accumulate(vals)[-1]) if len(vals) else 0.0
-
-
-def _first_crossing(vals, t):
-    """Index of the first running sum (left to right) that exceeds t, with that sum's start
-    value; (-1, _) if none."""
-    run = 0.0
-    for i, v in enumerate(vals):
-        nxt = run + v
-        if nxt > t:
-            return i, run
-        run = nxt
-    return -1, run
-
-
-def _last_positive(vals):
-    pos = np.nonzero(np.asarray(vals) > 0.0)[0]
-    return int(pos[-1]) if pos.size else -1
+def _exact_int(v: float) -> int:
+    """v * 2^SCALE_BITS as an exact integer (v >= 0 a multiple of 2^-SCALE_BITS)."""
+    m, e = float(v).as_integer_ratio()          # v = m / e exactly, e a power of two
+    q, r = divmod(m << SCALE_BITS, e)
+    if r:
+        raise ValueError(f"D² {v!r} is not a multiple of 2^-{SCALE_BITS}")
+    return q
 
 
 def draw(D2, u):
-    """The row drawn for uniform u (reading B9); -1 if every D² is 0.
-
-    Order of every sum: rows of a block (BLOCK rows) in row order; blocks of a group (GROUP
-    blocks) in block order; groups in group order.  The target u·total is located by running
-    sums at each level, top-down; where rounding leaves no crossing, the last positive entry."""
-    n = D2.shape[0]
-    nb = (n + BLOCK - 1) // BLOCK
-    ng = (nb + GROUP - 1) // GROUP
-    bsum = [_seq_sum(D2[b * BLOCK:(b + 1) * BLOCK]) for b in range(nb)]
-    gsum = [_seq_sum(bsum[g * GROUP:(g + 1) * GROUP]) for g in range(ng)]
-    total = _seq_sum(gsum)
-    target = u * total
-    g, R = _first_crossing(gsum, target)
-    scan = g >= 0
-    if not scan:
-        g = _last_positive(gsum)
-        if g < 0:
-            return -1
-    gb = bsum[g * GROUP:(g + 1) * GROUP]
-    if scan:
-        t1 = target - R
-        bi, P = _first_crossing(gb, t1)
-        scan = bi >= 0
-    if not scan:
-        bi = _last_positive(gb)
-    b = g * GROUP + bi
-    blk = D2[b * BLOCK:(b + 1) * BLOCK]
-    if scan:
-        t2 = t1 - P
-        run = 0.0
-        for i in range(blk.shape[0]):
-            run = run + blk[i]
-            if blk[i] > 0.0 and run > t2:
-                return b * BLOCK + i
-    return b * BLOCK + _last_positive(blk)
+    """The row drawn for uniform u (reading B9): the first i with exact Σ_{j<=i} D² > u Σ D²;
+    -1 if every D² is 0.  u·total is exact: u = mu / 2^s, so P_i > u·T <=> P_i > floor(mu·T / 2^s)
+    for integer P_i."""
+    ints = [_exact_int(v) for v in np.asarray(D2, np.float64).tolist()]
+    prefix = list(accumulate(ints))
+    total = prefix[-1] if prefix else 0
+    if total == 0:
+        return -1
+    mu, den = float(u).as_integer_ratio()       # u = mu / den, den = 2^s
+    target = (mu * total) // den
+    for i, p in enumerate(prefix):               # first crossing (always exists: u < 1)
+        if p > target:
+            return i
+    raise AssertionError("no crossing with u < 1")
 
 
 def seed_plusplus(X, k, uniforms, first_index):
@@ -101,7 +75,8 @@ def seed_plusplus(X, k, uniforms, first_index):
 
 
 def kmeanspp_multirun(X, k, runs, max_iters, tol=0):
-    """PAPER.md §4.3: r seeded runs of Lloyd's, the one with the smallest SSE (earlier on ties)."""
+    """PAPER.md §4.3: r seeded runs of Lloyd's, the one with the smallest SSE (the earliest on
+    ties).  Returns (index, a, C, sse, iterations) of the kept run."""
     from .oracle import lloyd
     best = None
     for i, (first, u) in enumerate(runs):

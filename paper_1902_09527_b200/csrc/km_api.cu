@@ -989,12 +989,12 @@ km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *poi
     KM_CUDA(cudaSetDevice(device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     float *Xd = nullptr, *crow = nullptr;
-    double *D2 = nullptr, *bsum = nullptr;
+    double *D2 = nullptr;
+    char *scratch = nullptr;
     int64_t *dsel = nullptr;
-    const int64_t nb = (n + 1023) / 1024, ng = (nb + 1023) / 1024;   // km_seed.cu block / group
     auto cleanup = [&]() {
         if (points_on_host) cudaFree(Xd);
-        cudaFree(crow); cudaFree(D2); cudaFree(bsum); cudaFree(dsel);
+        cudaFree(crow); cudaFree(D2); cudaFree(scratch); cudaFree(dsel);
     };
     km_status s = KM_OK;
     do {
@@ -1008,10 +1008,11 @@ km_status kmeans_seed_plusplus(int64_t n, int32_t d, int32_t k, const float *poi
         }
         if ((s = dalloc(&crow, (size_t)d)) != KM_OK) break;
         if ((s = dalloc(&D2, (size_t)n)) != KM_OK) break;
-        if ((s = dalloc(&bsum, (size_t)(nb + ng))) != KM_OK) break;
+        if ((s = dalloc(&scratch, km::seed_scratch_bytes(n))) != KM_OK) break;
         if ((s = dalloc(&dsel, (size_t)1)) != KM_OK) break;
-        cudaError_t e = km::seed_plusplus(Xd, n, d, d, k, first_index, uniforms, D2, bsum, crow, dsel, chosen, st);
+        cudaError_t e = km::seed_plusplus(Xd, n, d, d, k, first_index, uniforms, D2, scratch, crow, dsel, chosen, st);
         if (e == cudaErrorInvalidValue) { s = fail(KM_EARG, "fewer than k distinct rows"); break; }
+        if (e == cudaErrorNotSupported) { s = fail(KM_EARG, "a D^2 outside the exact fixed point (non-fp32 data)"); break; }
         if (e != cudaSuccess) { s = fail(KM_ECUDA, "seed_plusplus: %s", cudaGetErrorString(e)); break; }
         std::vector<float> row((size_t)d);
         for (int m = 0; m < k; ++m) {

@@ -140,8 +140,9 @@ cudaError_t launch_iota(int32_t *perm, int64_t n, cudaStream_t st);
 cudaError_t launch_pad_rows(const float *X, float *Xp, int64_t n, int d, int DP, cudaStream_t st);
 cudaError_t launch_check_finite(const float *X, int64_t count, int *flag, cudaStream_t st);
 cudaError_t launch_normalize_rows(float *X, int64_t n, int d, int DP, int *flag, cudaStream_t st);
+size_t seed_scratch_bytes(int64_t n);
 cudaError_t seed_plusplus(const float *X, int64_t n, int d, int ldx, int k, int64_t first,
-                          const double *u, double *D2, double *bsum, float *crow, int64_t *dsel,
+                          const double *u, double *D2, void *scratch, float *crow, int64_t *dsel,
                           int64_t *chosen, cudaStream_t st);
 
 }  // namespace km

@@ -285,10 +285,11 @@ def test_skmeans_zero_row_rejected():
 
 
 # ---- k-means++ D² seeding (Eq. 2) ---------------------------------
-@pytest.mark.parametrize("cfg,n", [("c1", None), ("c2", None), ("c3", 2_000_000)])
+@pytest.mark.parametrize("cfg,n", [("c1", None), ("c2", 200_000), ("c3", 300_000)])
 def test_seed_plusplus_matches_oracle(cfg, n):
-    """The GPU draws the same rows as the oracle for the same uniforms (reading B9), from device
-    and from host memory; the seeded run then matches the oracle's Lloyd from those centroids."""
+    """The GPU draws the same rows as the oracle for the same uniforms (reading B9: the first row
+    whose exact prefix sum of D² exceeds u times the exact total), from device and from host
+    memory; the seeded run then matches the oracle's Lloyd from those centroids."""
     from paper_1902_09527_b200 import seed_plusplus
     X, _, spec = make_config(cfg, n=n)
     k = spec["k"]
@@ -304,6 +305,27 @@ def test_seed_plusplus_matches_oracle(cfg, n):
     if cfg == "c1":
         r = oracle.lloyd(X, C_o, 100, 0, "mti")
         assert_strict(gpu_run(X, C_g, 100), r)
+
+
+def test_seed_plusplus_exact_crossing():
+    """D² = (0, 2^53, 1, 1) from fp32 rows (0,0), (2^26,2^26), (1,0), (0,1), first row 0, u the
+    largest double below 1: the exact target 2^53 + 1 - 2^-52 is first exceeded at row 2 (fp64
+    running sums, which round 2^53 + 1 to 2^53, would give row 1 or 3)."""
+    from paper_1902_09527_b200 import seed_plusplus
+    X = np.array([[0, 0], [2.0 ** 26, 2.0 ** 26], [1, 0], [0, 1]], np.float32)
+    u = [float(np.nextafter(1.0, 0.0))]
+    ch_o, _ = oracle.seed_plusplus(X, 2, u, 0)
+    ch_g, _ = seed_plusplus(torch.from_numpy(X).cuda(), 2, u, 0)
+    assert ch_o.tolist() == [0, 2] and ch_g.tolist() == [0, 2]
+    # the same at scale: 3 M rows of unit weight behind one row of weight 2^53
+    n = 3_000_000
+    Xb = np.zeros((n, 2), np.float32)
+    Xb[1] = 2.0 ** 26
+    Xb[2:, 0] = 1.0
+    ch_g, _ = seed_plusplus(torch.from_numpy(Xb).cuda(), 2, u, 0)
+    # exact: total T = 2^53 + n - 2, u T = 2^53 + n - 3 - (n - 2) 2^-53; the prefix through row
+    # i >= 1 is 2^53 + i - 1, first above u T at i = n - 2
+    assert ch_g.tolist() == [0, n - 2]
 
 
 def test_seed_plusplus_errors():

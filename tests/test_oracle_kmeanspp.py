@@ -41,9 +41,47 @@ def test_draw_law_matches_d2_weights():
     assert np.allclose(counts / len(us), D2 / D2.sum(), atol=1e-4)
 
 
-def test_block_boundaries():
-    """Rows spread over several blocks and groups: the draw lands where the cumulative weight
-    crosses u·total (brute-force cumulative sum over all rows)."""
+def _fraction_draw(D2, u):
+    """Eq. 2 with reading B9 in exact rationals: the first i with sum_{j<=i} D2_j > u * sum D2."""
+    from fractions import Fraction
+    vals = [Fraction(float(v)) for v in D2]
+    target = Fraction(float(u)) * sum(vals)
+    run = Fraction(0)
+    for i, v in enumerate(vals):
+        run += v
+        if run > target:
+            return i
+    return -1
+
+
+def test_draw_equals_exact_rational_definition():
+    """Rows with D² over a wide exponent range (and zeros), many u: the oracle's integer sums
+    pick the row the exact rational definition picks."""
+    rng = np.random.default_rng(1)
+    for trial in range(40):
+        n = int(rng.integers(1, 300))
+        D2 = rng.random(n) * np.exp2(rng.integers(-60, 60, n).astype(float))
+        D2[rng.random(n) < 0.2] = 0.0
+        if not (D2 > 0).any():
+            D2[0] = 1.0
+        for u in [0.0, float(rng.random()), float(rng.random()), np.nextafter(1.0, 0.0)]:
+            assert oracle.kmeanspp.draw(D2, u) == _fraction_draw(D2, u), (trial, u)
+
+
+def test_draw_is_exact_where_fp64_sums_are_not():
+    """D² = (2^53, 1, 1): the fp64 total rounds to 2^53, but the exact one is 2^53 + 2; with the
+    largest u below 1 the exact target 2^53 + 1 - 2^-52 is crossed first by row 1 (an fp64
+    running-sum implementation would answer row 0)."""
+    D2 = np.array([2.0 ** 53, 1.0, 1.0])
+    u = float(np.nextafter(1.0, 0.0))
+    assert oracle.kmeanspp.draw(D2, u) == 1
+    assert oracle.kmeanspp.draw(np.array([1.0, 2.0, 3.0]), 0.5) == 2                 # P = 3 is not > 3
+    assert oracle.kmeanspp.draw(np.array([1.0, 2.0, 3.0]), float(np.nextafter(0.5, 0.0))) == 1
+    assert oracle.kmeanspp.draw(np.array([0.0, 0.0, 5.0, 0.0]), 0.0) == 2             # zeros never drawn
+
+
+def test_large_array_matches_cumsum():
+    """Two million rows: the exact draw agrees with an fp64 cumulative sum up to its rounding."""
     rng = np.random.default_rng(1)
     n = 2 * 1024 * 1024 + 3 * 1024 + 123
     D2 = rng.random(n) ** 4
@@ -51,7 +89,24 @@ def test_block_boundaries():
     for u in [0.0, 0.1, 0.3333, 0.5, 0.77, 0.999999]:
         i = oracle.kmeanspp.draw(D2, u)
         j = int(np.searchsorted(tot, u * tot[-1], side="right"))
-        assert abs(i - j) <= 1, (u, i, j)       # equal up to fp64 rounding of the two sums
+        assert abs(i - j) <= 1, (u, i, j)
+
+
+def test_multirun_hand_case():
+    """PAPER.md §4.3 best-of-r, hand-checked.  Rectangle (0,0), (0,1), (4,0), (4,1), k = 2, first
+    row 0, D² = (0, 1, 16, 17), total 34.  Run A (u = 0.01, target 0.34): row 1 -> centres
+    (0,0), (0,1) -> Lloyd's fixed point {(0,0),(4,0)} / {(0,1),(4,1)}: C = (2,0), (2,1), SSE 16.
+    Run B (u = 0.5, target 17): row 3 -> centres (0,0), (4,1) -> {(0,0),(0,1)} / {(4,0),(4,1)}:
+    C = (0,0.5), (4,0.5), SSE 1.  The best of (A, B) is B; of (B, A) it is B again (index 0);
+    of (A, A) the first."""
+    X = np.array([[0, 0], [0, 1], [4, 0], [4, 1]], np.float32)
+    A, B = (0, [0.01]), (0, [0.5])
+    i, a, C, sse, it = oracle.kmeanspp_multirun(X, 2, [A, B], 20)
+    assert i == 1 and sse == 1.0 and C.tolist() == [[0.0, 0.5], [4.0, 0.5]] and a.tolist() == [0, 0, 1, 1]
+    i, _, _, sse, _ = oracle.kmeanspp_multirun(X, 2, [B, A], 20)
+    assert i == 0 and sse == 1.0
+    i, a, C, sse, _ = oracle.kmeanspp_multirun(X, 2, [A, A], 20)
+    assert i == 0 and sse == 16.0 and C.tolist() == [[2.0, 0.0], [2.0, 1.0]] and a.tolist() == [0, 1, 0, 1]
 
 
 def test_multirun_keeps_min_sse():
