@@ -231,7 +231,7 @@ def test_enumerator_matches_1d_dp(seed):
     assert abs(e - _opt_dp_1d(x, 3)) < 1e-12
 
 
-@pytest.mark.parametrize("seed,n,k,d", [(0, 9, 3, 2), (1, 10, 3, 2), (2, 8, 4, 3)])
+@pytest.mark.parametrize("seed,n,k,d", [(0, 9, 3, 2), (1, 10, 3, 2), (2, 8, 4, 3), (3, 12, 3, 2)])
 def test_lloyd_vs_global_optimum(seed, n, k, d):
     X = np.random.default_rng(seed).normal(size=(n, d)).astype(np.float32)
     opt, lab = _opt_enum(X, k)
