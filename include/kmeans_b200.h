@@ -60,11 +60,15 @@ enum { KM_PRUNE_MTI = 0, KM_PRUNE_NONE = 1, KM_PRUNE_TI = 2 };
 enum { KM_RESORT_AUTO = 0, KM_RESORT_NEVER = 1, KM_RESORT_ALWAYS = 2 };
 
 /* Candidate-evaluation engine of the MTI pass.  AUTO and CUDA_CORE: the CUDA-core
- * walk ("k_walk"; "k_walk_skip1" when the previous pass's clause-1 rate exceeds 15 %).  TENSOR:
- * the tcgen05 TF32x3 kernel ("k_mti_tc"; d padded to 8, 16 or 32; measured slower, opt-in).  All
- * give the same (exact-mode) assignments.  Iteration 1 and KM_PRUNE_NONE always use the
- * CUDA-core dense kernel. */
-enum { KM_ENGINE_AUTO = 0, KM_ENGINE_CUDA_CORE = 1, KM_ENGINE_TENSOR = 2 };
+ * walk ("k_walk"; "k_walk_skip1" when the previous pass's clause-1 rate exceeds 15 %).  SCREEN:
+ * the same walk split in two kernels ("k_screen": every row, minimum candidate value only, the
+ * rows that provably stay are decided; "k_resolve": the queued rest, direct form + exact-mode
+ * decision).  TENSOR: the tcgen05 TF32x3 kernel ("k_mti_tc"; d padded to 8, 16 or 32; measured
+ * slower, opt-in).  TENSOR_SCREEN: the tcgen05 kernel screening (smallest column value only, rows
+ * that provably stay decided; "k_mti_tc_screen") followed by k_resolve.  All give the same (exact-mode) assignments.  Iteration 1 and KM_PRUNE_NONE
+ * always use the CUDA-core dense kernel. */
+enum { KM_ENGINE_AUTO = 0, KM_ENGINE_CUDA_CORE = 1, KM_ENGINE_TENSOR = 2, KM_ENGINE_SCREEN = 3,
+       KM_ENGINE_TENSOR_SCREEN = 4 };
 
 typedef struct km_options {
     int32_t device;            /* CUDA device ordinal the context lives on */

@@ -172,6 +172,7 @@ struct km_ctx {
     double *sse_buf = nullptr;
     int32_t *a_out = nullptr;
     double *exact_P = nullptr;      // exact-order sums: per 64 Ki-row block x cluster partials (B12)
+    bool perm_identity = true;      // stored rows still in caller order (no re-bucketing yet)
     HostStat *hstat = nullptr;
     int grid_assign[4] = {0, 0, 0, 0};
     float g_up = 1.f, g_dn = 1.f;
@@ -199,6 +200,11 @@ struct km_ctx {
     // NEXT-2: the walk reads only the rows that fail clause 1, chosen when the last pass's
     // clause-1 rate exceeded kSkip1Rate (global counts: the same choice on every rank)
     bool skip1 = false;
+    // screen engine (km_screen.cu): k_screen decides the rows that stay, k_resolve the queued rest
+    bool use_screen = false;        // CUDA-core screen (k_screen) or, with use_tc, tensor screen
+    int *qrow = nullptr, *qcnt = nullptr;   // per 32-row group: queued rows, count
+    int16_t *nlrank = nullptr;      // tensor screen: k x k neighbour-list positions
+    int screen_grid = 0, resolve_grid = 0;
     int64_t launches = 0;
 };
 
@@ -231,7 +237,8 @@ km_status prep(km_ctx *c)
         c->launches += 1;
     }
     if (c->use_tc) {
-        KM_CUDA(km::launch_prep_tc(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->tc_nmax, c->Bop, c->Bmeta, c->st));
+        KM_CUDA(km::launch_prep_tc(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->tc_nmax, c->Bop, c->Bmeta,
+                                   c->use_screen ? c->nlrank : nullptr, c->st));
         c->launches += 1;
     }
     return KM_OK;
@@ -276,6 +283,9 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
     p.whs = c->whs;
     p.wpad = c->wpad;
     p.wbits = c->wbits;
+    p.qrow = c->qrow;
+    p.qcnt = c->qcnt;
+    p.rank = c->nlrank;
     return p;
 }
 
@@ -285,9 +295,19 @@ km_status launch_assign(km_ctx *c, int mode, int work_slot)
     if (c->use_ti && (mode == km::MODE_MTI_REDUCE || mode == km::MODE_DENSE)) {
         KM_CUDA(km::launch_ti(c->DP, c->csmem, mode == km::MODE_DENSE, p, c->L, c->Hm, c->ti_grid, c->st));
     } else if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
-        if (c->use_tc) KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->st));
-        else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->skip1, c->st));
-        if (c->use_tc || !c->wh_smem) {   // deferred distance counts (misfit rows)
+        if (c->use_tc) {
+            KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->use_screen, c->st));
+            if (c->use_screen) {
+                KM_CUDA(km::launch_resolve(c->DP, c->csmem, p, c->resolve_grid, c->st));
+                c->launches += 1;
+            }
+        }
+        else if (c->use_screen) {
+            KM_CUDA(km::launch_screen(c->DP, c->csmem, p, c->screen_grid, c->resolve_grid, c->skip1, c->qrow, c->qcnt,
+                                      c->n_alloc, c->st));
+            c->launches += 1;
+        } else KM_CUDA(km::launch_walk(c->DP, c->csmem, p, c->walk_grid, c->skip1, c->st));
+        if (!c->use_screen && (c->use_tc || !c->wh_smem)) {   // deferred distance counts (misfit rows)
             KM_CUDA(km::launch_mti_count(c->defer, c->dcount, c->n_alloc / 128, c->counters, c->NL, c->ks, c->k,
                                          c->num_sms, c->st));
             c->launches += 1;
@@ -323,6 +343,7 @@ km_status resort(km_ctx *c)
     KM_CUDA(km::launch_sort(p, c->st, &l));
     c->launches += l;
     c->cur = nw;
+    c->perm_identity = false;
     c->changed_since_sort = 0;
     c->last_sort_t = c->t;
     return KM_OK;
@@ -336,7 +357,7 @@ km_status exact_sums(km_ctx *c)
     int l = 0;
     KM_CUDA(km::launch_exact_sums(c->X[c->cur], c->a[c->cur], c->perm[c->cur], c->n, c->DP, c->k,
                                   reinterpret_cast<int32_t *>(c->keys), c->a[1 - c->cur], c->exact_P, c->acc,
-                                  c->st, &l));
+                                  c->perm_identity, c->st, &l));
     c->launches += l;
     return KM_OK;
 }
@@ -462,11 +483,13 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
         KM_CUDA(cudaEventRecord(ev[2], c->st));
         KM_TRY(launch_assign(c, km::MODE_DENSE, 0));
         KM_CUDA(cudaEventRecord(ev[3], c->st));
+        // the full reduction first, while the rows are still in caller order (no permutation to
+        // invert: reading B12's order is the stored order), then the first re-bucketing
+        KM_TRY(exact_sums(c));
         if (c->resort_policy != KM_RESORT_NEVER) {
             KM_TRY(resort(c));
             sorted_now = true;
         }
-        KM_TRY(exact_sums(c));
         KM_CUDA(cudaEventRecord(ev[4], c->st));
         KM_TRY(allreduce(c));
         KM_CUDA(cudaEventRecord(ev[5], c->st));
@@ -529,7 +552,7 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base); cudaFree(c->lohist); cudaFree(c->qmap);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P);
+    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P); cudaFree(c->qrow); cudaFree(c->qcnt); cudaFree(c->nlrank);
     cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part); cudaFree(c->L); cudaFree(c->Hm);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -677,16 +700,16 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     }
     // AUTO: the CUDA-core walk (measured faster than the tensor-core pipeline on C3 and C4 so
     // far); KM_ENGINE_TENSOR selects the tcgen05 kernel
-    c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 && !c->use_ti &&
-                o->engine == KM_ENGINE_TENSOR;
-    if (o->engine == KM_ENGINE_TENSOR && !km::tc_supported(DP))
+    const bool want_tc = o->engine == KM_ENGINE_TENSOR || o->engine == KM_ENGINE_TENSOR_SCREEN;
+    c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 && !c->use_ti && want_tc;
+    if (want_tc && !km::tc_supported(DP))
         return fail(KM_EARG, "tensor engine needs d padded to 8, 16 or 32 (d=%d)", d);
     // the tensor-core kernel handles rows outside the tile's cluster without extra walks, so
     // re-bucketing only pays when the layout is badly mixed
     if (c->use_tc) {
         c->tc_nmax = std::min(256, std::max(16, (k - 1 + 15) & ~15));   // columns: NL[A] prefix
         if (km::tc_plan(DP, c->csmem, k, c->tc_nmax, c->num_sms, &c->tc_grid, &c->tc_cols) == 0) {
-            if (o->engine == KM_ENGINE_TENSOR)
+            if (want_tc)
                 return fail(KM_EARG, "tensor engine: shared memory for d=%d k=%d exceeds one SM", d, k);
             c->use_tc = false;
         }
@@ -696,6 +719,14 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         KM_TRY(dalloc(&c->Bop, (size_t)k * c->tc_nmax * KT));
         KM_TRY(dalloc(&c->Bmeta, (size_t)k * km::tc_nmeta_host(c->tc_nmax)));
         c->part_grid = std::max(c->part_grid, c->tc_grid);
+        if (o->engine == KM_ENGINE_TENSOR_SCREEN) {
+            c->use_screen = true;
+            c->resolve_grid = km::resolve_grid(DP, c->csmem, k, c->num_sms);
+            KM_TRY(dalloc(&c->qrow, (size_t)c->n_alloc));
+            KM_TRY(dalloc(&c->qcnt, (size_t)(c->n_alloc / 32)));
+            KM_TRY(dalloc(&c->nlrank, (size_t)k * k));
+            c->part_grid = std::max(c->part_grid, c->resolve_grid);
+        }
     }
     // CUDA-core engine: the centred expansion-form walk (k_walk); KM_ENGINE_CUDA_CORE with a
     // compile-time -DKM_LEGACY_WALK keeps the direct-form lane walk of k_assign (A/B builds only)
@@ -728,6 +759,13 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         KM_TRY(dalloc(&c->WH, (size_t)k * c->whs));
         c->walk_grid = km::walk_grid(DP, c->csmem, k, c->whs, c->wh_smem, c->num_sms);
         c->part_grid = std::max(c->part_grid, c->walk_grid);
+        c->use_screen = o->engine == KM_ENGINE_SCREEN;
+        if (c->use_screen) {
+            km::screen_grids(DP, c->csmem, k, c->whs, c->wh_smem, c->num_sms, &c->screen_grid, &c->resolve_grid);
+            KM_TRY(dalloc(&c->qrow, (size_t)c->n_alloc));
+            KM_TRY(dalloc(&c->qcnt, (size_t)(c->n_alloc / 32)));
+            c->part_grid = std::max(c->part_grid, std::max(c->screen_grid, c->resolve_grid));
+        }
     }
     if (c->use_tc || c->use_walk) {
         KM_TRY(dalloc(&c->defer, (size_t)c->n_alloc));
@@ -960,7 +998,8 @@ const char *kmeans_engine(const km_ctx *c)
     if (!c) return "";
     if (c->prune == KM_PRUNE_NONE) return "k_assign_dense";
     if (c->use_ti) return "k_ti";
-    return c->use_tc ? "k_mti_tc" : (c->use_walk ? "k_walk" : "k_assign");
+    if (c->use_tc && c->use_screen) return "k_mti_tc_screen";
+    return c->use_tc ? "k_mti_tc" : (c->use_walk ? (c->use_screen ? "k_screen" : "k_walk") : "k_assign");
 }
 
 void kmeans_destroy(km_ctx *c)

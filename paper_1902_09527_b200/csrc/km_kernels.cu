@@ -498,6 +498,139 @@ __global__ void __launch_bounds__(kExactThreads) k_exact_block_sums(const float 
     }
 }
 
+// The same sums as k_exact_block_sums, one CTA per 64 Ki-row block (k <= kExactListK), in four
+// sub-blocks of 16 Ki rows taken in row order.  Per sub-block: a stable counting sort of its rows
+// by cluster in shared memory (kExactSortWarps warps, each over a contiguous eighth: per-warp
+// counts, an exclusive scan in (cluster, warp) order, then each warp places its rows in row
+// order), so every cluster's rows form one list in row order; then one thread per (cluster,
+// coordinate) continues its sequential fp64 sum (kept in P between sub-blocks) over its list.
+// Bit-identical to k_exact_block_sums (the same additions in the same order), without every
+// thread scanning all 65536 assignments of the block.  inv == nullptr: caller order = stored order.
+constexpr int kExactListK = 1024;
+constexpr int kExactSortWarps = 8;
+constexpr int kExactListThreads = 512;
+constexpr int kExactSub = 16384;
+
+__host__ __device__ constexpr size_t exact_list_smem(int k)
+{
+    return (size_t)kExactSub * sizeof(uint16_t) + (size_t)(kExactSortWarps + 2) * k * sizeof(int) + 32 * sizeof(int);
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kExactListThreads) k_exact_list_sums(const float *X, const int32_t *inv,
+                                                                      const int32_t *ac, int64_t n, int k,
+                                                                      double *P)
+{
+    extern __shared__ __align__(16) uint8_t esm[];
+    uint16_t *list = reinterpret_cast<uint16_t *>(esm);                       // kExactSub row offsets
+    int *cnt = reinterpret_cast<int *>(esm + kExactSub * sizeof(uint16_t));    // [warp][cluster] -> offsets
+    int *cbase = cnt + kExactSortWarps * k;                                     // cluster list start
+    int *ctot = cbase + k;                                                      // cluster row count
+    int *wsum = ctot + k;                                                       // scan scratch (32 ints)
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int nw = (int)(blockDim.x >> 5);
+    constexpr int kSpan = kExactSub / kExactSortWarps;      // rows per sort warp
+    constexpr int U = 8;                                    // assignment loads in flight per lane
+    for (int sub = 0; sub < (int)(kExactBlock / kExactSub); ++sub) {
+        const int64_t r0 = (int64_t)blockIdx.x * kExactBlock + (int64_t)sub * kExactSub;
+        if (r0 >= n) break;
+        const int m = (int)(n - r0 < kExactSub ? n - r0 : kExactSub);
+        for (int i = tid; i < kExactSortWarps * k; i += blockDim.x) cnt[i] = 0;
+        __syncthreads();
+        const int w0 = w * kSpan, w1 = min(m, w0 + kSpan);
+        if (w < kExactSortWarps) {                       // per-warp counts
+            int *cw = cnt + w * k;
+            for (int b = w0; b < w1; b += 32 * U) {
+                int cv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) { const int i = b + 32 * u + lane; cv[u] = i < w1 ? ac[r0 + i] : -1; }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const unsigned g = __match_any_sync(kFull, cv[u]);
+                    if (cv[u] >= 0 && lane == __ffs(g) - 1) cw[cv[u]] += __popc(g);
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+        // cluster totals and their exclusive scan (cluster order), then per-warp offsets
+        int run = 0;
+        for (int c0 = 0; c0 < k; c0 += blockDim.x) {
+            const int c = c0 + tid;
+            int t = 0;
+            if (c < k)
+                for (int ww = 0; ww < kExactSortWarps; ++ww) t += cnt[ww * k + c];
+            int incl = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (lane == 31) wsum[w] = incl;
+            __syncthreads();
+            int wpre = 0, tot = 0;
+            for (int ww = 0; ww < nw; ++ww) { wpre += ww < w ? wsum[ww] : 0; tot += wsum[ww]; }
+            if (c < k) {
+                const int base = run + wpre + incl - t;
+                cbase[c] = base;
+                ctot[c] = t;
+                int o = base;
+                for (int ww = 0; ww < kExactSortWarps; ++ww) {
+                    const int v = cnt[ww * k + c];
+                    cnt[ww * k + c] = o;
+                    o += v;
+                }
+            }
+            run += tot;
+            __syncthreads();
+        }
+        if (w < kExactSortWarps) {                       // stable placement, row order per warp
+            int *cw = cnt + w * k;
+            for (int b = w0; b < w1; b += 32 * U) {
+                int cv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) { const int i = b + 32 * u + lane; cv[u] = i < w1 ? ac[r0 + i] : -1; }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = cv[u];
+                    const unsigned g = __match_any_sync(kFull, c);
+                    if (c >= 0) list[cw[c] + __popc(g & ((1u << lane) - 1u))] = (uint16_t)(b + 32 * u + lane);
+                    __syncwarp();
+                    if (c >= 0 && lane == __ffs(g) - 1) cw[c] += __popc(g);
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+        // sequential fp64 sums, one thread per (cluster, coordinate) (+ the count), continued
+        // from the previous sub-block's value in P
+        for (int item = tid; item < k * (DP + 1); item += blockDim.x) {
+            const int c = item / (DP + 1), j = item % (DP + 1);
+            double *pb = P + ((int64_t)blockIdx.x * k + c) * (DP + 1);
+            const int t0 = cbase[c], t1 = t0 + ctot[c];
+            if (j == DP) { pb[DP] = (sub ? pb[DP] : 0.0) + (double)(t1 - t0); continue; }
+            double s = sub ? pb[j] : 0.0;
+            int t = t0;
+            for (; t + U <= t1; t += U) {                // U loads in flight, adds in row order
+                float v[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int64_t row = r0 + list[t + q];
+                    v[q] = __ldg(X + (int64_t)(inv ? inv[row] : row) * DP + j);
+                }
+#pragma unroll
+                for (int q = 0; q < U; ++q) s = __dadd_rn(s, (double)v[q]);
+            }
+            for (; t < t1; ++t) {
+                const int64_t row = r0 + list[t];
+                s = __dadd_rn(s, (double)__ldg(X + (int64_t)(inv ? inv[row] : row) * DP + j));
+            }
+            pb[j] = s;
+        }
+        __syncthreads();
+    }
+}
+
 // acc[c][j] = ((0 + P_0[c][j]) + P_1[c][j]) + ... in block order
 __global__ void k_exact_merge(const double *P, int64_t nblk, int64_t elems, double *acc)
 {
@@ -510,13 +643,49 @@ __global__ void k_exact_merge(const double *P, int64_t nblk, int64_t elems, doub
 
 int64_t exact_blocks(int64_t n) { return (n + kExactBlock - 1) / kExactBlock; }
 
+template <int DP>
+static cudaError_t launch_exact_list(const float *X, const int32_t *inv, const int32_t *ac, int64_t n, int k,
+                                     double *P, cudaStream_t st)
+{
+    const size_t sm = exact_list_smem(k);
+    cudaError_t e = cudaFuncSetAttribute(k_exact_list_sums<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_exact_list_sums<DP><<<(unsigned)exact_blocks(n), kExactListThreads, sm, st>>>(X, inv, ac, n, k, P);
+    return cudaGetLastError();
+}
+
+// identity: the stored rows are in caller order (perm = iota, before the first re-bucketing), so
+// the assignments and rows are read in place
 cudaError_t launch_exact_sums(const float *X, const int32_t *a, const int32_t *perm, int64_t n, int DP, int k,
-                              int32_t *inv, int32_t *ac, double *P, double *acc, cudaStream_t st, int *launches)
+                              int32_t *inv, int32_t *ac, double *P, double *acc, bool identity, cudaStream_t st,
+                              int *launches)
 {
     const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    k_inv_perm<<<g, 256, 0, st>>>(perm, n, inv);
-    k_unpermute<<<g, 256, 0, st>>>(a, perm, n, ac);
+    if (k > kExactListK) identity = false;   // the scan kernel reads through inv
+    if (identity) {
+        inv = nullptr;
+        ac = const_cast<int32_t *>(a);
+    } else {
+        k_inv_perm<<<g, 256, 0, st>>>(perm, n, inv);
+        k_unpermute<<<g, 256, 0, st>>>(a, perm, n, ac);
+        *launches += 2;
+    }
     const int64_t nblk = exact_blocks(n);
+    const int64_t elems = (int64_t)k * (DP + 1);
+    if (k <= kExactListK) {
+        cudaError_t e = cudaErrorInvalidValue;
+        switch (DP) {
+        case 4: e = launch_exact_list<4>(X, inv, ac, n, k, P, st); break;
+        case 8: e = launch_exact_list<8>(X, inv, ac, n, k, P, st); break;
+        case 16: e = launch_exact_list<16>(X, inv, ac, n, k, P, st); break;
+        case 32: e = launch_exact_list<32>(X, inv, ac, n, k, P, st); break;
+        case 64: e = launch_exact_list<64>(X, inv, ac, n, k, P, st); break;
+        }
+        if (e != cudaSuccess) return e;
+        k_exact_merge<<<(unsigned)((elems + 255) / 256), 256, 0, st>>>(P, nblk, elems, acc);
+        *launches += 2;
+        return cudaGetLastError();
+    }
     const dim3 grid((unsigned)nblk, (unsigned)((k + kExactThreads - 1) / kExactThreads));
     switch (DP) {
     case 4: k_exact_block_sums<4><<<grid, kExactThreads, 0, st>>>(X, inv, ac, n, k, P); break;
@@ -526,9 +695,8 @@ cudaError_t launch_exact_sums(const float *X, const int32_t *a, const int32_t *p
     case 64: k_exact_block_sums<64><<<grid, kExactThreads, 0, st>>>(X, inv, ac, n, k, P); break;
     default: return cudaErrorInvalidValue;
     }
-    const int64_t elems = (int64_t)k * (DP + 1);
     k_exact_merge<<<(unsigned)((elems + 255) / 256), 256, 0, st>>>(P, nblk, elems, acc);
-    *launches += 4;
+    *launches += 2;
     return cudaGetLastError();
 }
 

@@ -70,6 +70,11 @@ struct AssignParams {
     int32_t wh_smem;       // 1: stage WH in shared memory
     int32_t wpad;          // candidate rows per cluster (>= k, even)
     int32_t wbits;         // key index bits (2^wbits >= wpad)
+    // screen engines (k_screen, k_mti_tc<SCREEN>) -> k_resolve: per 32-row group g,
+    // qrow[32 g .. 32 g + qcnt[g]) = the rows left undecided
+    int *qrow;
+    int *qcnt;
+    const int16_t *rank;   // k x k: position of c' in c's neighbour list (tensor-screen epilogue)
 };
 
 struct PrepParams {
@@ -110,9 +115,11 @@ cudaError_t launch_partials_reduce(const double *part, int parts, int64_t elems,
 bool tc_supported(int DP);
 int tc_kt_host(int DP);
 size_t tc_plan(int DP, bool csmem, int k, int nmax, int num_sms, int *grid, int *tmem_cols);
-cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st);
+cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, bool screen, cudaStream_t st);
 cudaError_t launch_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
-                           float *Bop, float4 *Bmeta, cudaStream_t st);
+                           float *Bop, float4 *Bmeta, int16_t *rank, cudaStream_t st);
+cudaError_t launch_resolve(int DP, bool csmem, const AssignParams &p, int g_resolve, cudaStream_t st);
+int resolve_grid(int DP, bool csmem, int k, int num_sms);
 cudaError_t launch_mti_count(const unsigned long long *defer, const int *dcount, int64_t ntiles,
                              unsigned long long *counters, const uint64_t *NL, int ks, int k, int num_sms,
                              cudaStream_t st);
@@ -120,6 +127,9 @@ int tc_nmeta_host(int nmax);
 bool walk_supported(int DP);
 cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, bool skip1, cudaStream_t st);
 int walk_grid(int DP, bool csmem, int k, int kp, bool whs, int num_sms);
+void screen_grids(int DP, bool csmem, int k, int whs, bool hs, int num_sms, int *g_screen, int *g_resolve);
+cudaError_t launch_screen(int DP, bool csmem, const AssignParams &p, int g_screen, int g_resolve, bool skip1,
+                          int *qrow, int *qcnt, int64_t n_alloc, cudaStream_t st);
 cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int kp, int whs,
                              float4 *Wblk, float *Wcc, float2 *Wmeta, float *WH, cudaStream_t st);
 int ti_grid(int DP, bool csmem, int k, int num_sms);
@@ -133,7 +143,8 @@ cudaError_t launch_sse(const float *X, const int32_t *a, const double *C, int64_
                        int DP, double *out, cudaStream_t st);
 int64_t exact_blocks(int64_t n);
 cudaError_t launch_exact_sums(const float *X, const int32_t *a, const int32_t *perm, int64_t n, int DP, int k,
-                              int32_t *inv, int32_t *ac, double *P, double *acc, cudaStream_t st, int *launches);
+                              int32_t *inv, int32_t *ac, double *P, double *acc, bool identity, cudaStream_t st,
+                              int *launches);
 cudaError_t launch_unpermute(const int32_t *a, const int32_t *perm, int64_t n, int32_t *out,
                              cudaStream_t st);
 cudaError_t launch_iota(int32_t *perm, int64_t n, cudaStream_t st);

@@ -217,7 +217,18 @@ __device__ __forceinline__ int count_below_nl(const uint64_t *nl, int m, float T
     return lo;
 }
 
-template <int DP, bool CSMEM, int NMETA>
+__device__ __forceinline__ float tc_fmin3(float a, float b, float c)
+{
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// SCREEN (the "tensor-screen" engine): the epilogue keeps only the smallest column value of each
+// row (the own column masked for rows of another cluster), decides the rows that provably stay
+// and queues the rest (p.qrow / p.qcnt per 32-row group) for k_resolve (km_screen.cu), which
+// takes the exact-mode decision and applies the moves.
+template <int DP, bool CSMEM, int NMETA, bool SCREEN>
 __global__ void __launch_bounds__(kTcThreads, 2)
 k_mti_tc(AssignParams p, TcCfg L)
 {
@@ -406,7 +417,8 @@ k_mti_tc(AssignParams p, TcCfg L)
             const bool misfit = active && aold != A;
             c_clause1 += c1;
             TcRow st;
-            st.a = aold; st.uu = uu; st.xx = 0.f; st.ut = 0.f; st.lo = 0.f; st.p = 0; st.pad = 0;
+            st.a = aold; st.uu = uu; st.xx = 0.f; st.ut = 0.f; st.lo = 0.f; st.p = 0; st.pad = -1;
+            if (SCREEN && misfit) st.pad = p.rank[(int64_t)A * k + aold];   // own column in A's list
             int flags = (valid ? 1 : 0) | (active ? 2 : 0) | (misfit ? 4 : 0);
             if (active) {
                 // x' = x - C^[A] in the direct form's arithmetic (x + (-c)), xx = |x'|^2
@@ -507,6 +519,56 @@ k_mti_tc(AssignParams p, TcCfg L)
             const bool valid = st.flags & 1, active = st.flags & 2, misfit = st.flags & 4;
             const bool uncovered = st.flags & 8;
             const float4 *meta = meta0 + inf.mslot * NMETA;
+            if constexpr (SCREEN) {
+                const int pw = inf.N > 0 ? inf.pw[ew] : 0;
+                const int own = st.pad;
+                float m = INFINITY;
+                for (int c0 = 0; c0 < pw; c0 += 16) {
+                    uint32_t rr[16];
+                    tc::tmem_ld16(tlane + (uint32_t)(b * NMAX + c0), rr);
+                    if (__any_sync(kFull, own >= c0 && own < c0 + 16)) {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q)
+                            if (c0 + q == own) rr[q] = 0x7f800000u;   // +inf: the own cluster is not a rival
+                    }
+#pragma unroll
+                    for (int q = 0; q < 16; q += 2) m = tc_fmin3(m, __uint_as_float(rr[q]), __uint_as_float(rr[q + 1]));
+                }
+                if (lane == 0) c_cols += (unsigned long long)pw;
+                const float cmax = pw > 0 ? meta[pw - 1].w : 0.f;
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_tfree[b]));   // TMEM / A / row state / metadata free
+                // stays iff every rival column's lower bound exceeds the own upper bound u_t
+                // (squared domain: m > (u_t + epsr)^2 + E) and, for a row of another cluster, the
+                // tile cluster A itself is farther than u_t
+                bool decided = false;
+                if (active && !uncovered) {
+                    const float E = __fmul_ru(kappa, __fadd_ru(st.xx, cmax));
+                    const float epsr = __fadd_ru(eps, __fmul_ru(1.2e-7f, __fadd_ru(sqrt_up(st.xx), sqrt_up(cmax))));
+                    const float ue = __fadd_ru(st.ut, epsr);
+                    const float thr = __fadd_ru(__fmul_ru(ue, ue), E);
+                    decided = m > thr && (!misfit || lower_d(st.xx, p.g_dn, eps) > st.ut);
+                    // MTI distance count 1 + #{c : H[a][c] < u_t}
+                    if (decided)
+                        c_dists += 1ull + (unsigned long long)(misfit ? count_below_nl(p.NL + (int64_t)st.a * p.ks, k - 1, st.ut)
+                                                                      : st.p);
+                }
+                const bool qd = active && !decided;
+                const unsigned qm = __ballot_sync(kFull, qd);
+                const int64_t grp = tile * 4 + ew;
+                if (tile * kTcRows + ew * 32 < n) {
+                    if (qd) p.qrow[grp * 32 + __popc(qm & ((1u << lane) - 1u))] = (int)row;
+                    if (lane == 0) p.qcnt[grp] = __popc(qm);
+                }
+                c_fb += qd;
+                // clause-1 rows keep the loosened bound, decided rows the tightened one (queued
+                // rows are rewritten by k_resolve)
+                if (valid) p.u[row] = decided ? st.ut : st.uu;
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_sfree[s]));     // stage reusable
+                continue;
+            }
             const float *sx = reinterpret_cast<const float *>(smem + L.ring + s * L.stage_bytes);
             float x[DP];
 #pragma unroll
@@ -717,23 +779,24 @@ static TcCfg pick_cfg(int DP, bool csmem, int k, int nmax, int optin, int smem_s
 }
 
 template <int DP, bool CSMEM, int NMETA>
-static cudaError_t launch_tc_t(const AssignParams &p, const TcCfg &L, int grid, cudaStream_t st)
+static cudaError_t launch_tc_t(const AssignParams &p, const TcCfg &L, int grid, bool screen, cudaStream_t st)
 {
-    cudaError_t e = cudaFuncSetAttribute(k_mti_tc<DP, CSMEM, NMETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+    auto kern = screen ? k_mti_tc<DP, CSMEM, NMETA, true> : k_mti_tc<DP, CSMEM, NMETA, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
     if (e != cudaSuccess) return e;
-    k_mti_tc<DP, CSMEM, NMETA><<<grid, kTcThreads, L.total, st>>>(p, L);
+    kern<<<grid, kTcThreads, L.total, st>>>(p, L);
     return cudaGetLastError();
 }
 
 template <int DP, bool CSMEM>
-static cudaError_t launch_tc_m(const AssignParams &p, const TcCfg &L, int grid, cudaStream_t st)
+static cudaError_t launch_tc_m(const AssignParams &p, const TcCfg &L, int grid, bool screen, cudaStream_t st)
 {
     switch (p.nmeta) {
-    case 16: return launch_tc_t<DP, CSMEM, 16>(p, L, grid, st);
-    case 32: return launch_tc_t<DP, CSMEM, 32>(p, L, grid, st);
-    case 64: return launch_tc_t<DP, CSMEM, 64>(p, L, grid, st);
-    case 128: return launch_tc_t<DP, CSMEM, 128>(p, L, grid, st);
-    case 256: return launch_tc_t<DP, CSMEM, 256>(p, L, grid, st);
+    case 16: return launch_tc_t<DP, CSMEM, 16>(p, L, grid, screen, st);
+    case 32: return launch_tc_t<DP, CSMEM, 32>(p, L, grid, screen, st);
+    case 64: return launch_tc_t<DP, CSMEM, 64>(p, L, grid, screen, st);
+    case 128: return launch_tc_t<DP, CSMEM, 128>(p, L, grid, screen, st);
+    case 256: return launch_tc_t<DP, CSMEM, 256>(p, L, grid, screen, st);
     }
     return cudaErrorInvalidValue;
 }
@@ -761,7 +824,7 @@ size_t tc_plan(int DP, bool csmem, int k, int nmax, int num_sms, int *grid, int 
     return ctas > 0 ? (size_t)L.total : 0;
 }
 
-cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, cudaStream_t st)
+cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, bool screen, cudaStream_t st)
 {
     int dev = 0, optin = 0, smem_sm = 0, ctas = 0;
     cudaGetDevice(&dev);
@@ -770,12 +833,12 @@ cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, c
     const TcCfg L = pick_cfg(DP, csmem, p.k, p.nmax, optin, smem_sm, &ctas);
     if (ctas == 0) return cudaErrorInvalidValue;
     switch (DP * 2 + (csmem ? 1 : 0)) {
-    case 16: return launch_tc_m<8, false>(p, L, grid, st);
-    case 17: return launch_tc_m<8, true>(p, L, grid, st);
-    case 32: return launch_tc_m<16, false>(p, L, grid, st);
-    case 33: return launch_tc_m<16, true>(p, L, grid, st);
-    case 64: return launch_tc_m<32, false>(p, L, grid, st);
-    case 65: return launch_tc_m<32, true>(p, L, grid, st);
+    case 16: return launch_tc_m<8, false>(p, L, grid, screen, st);
+    case 17: return launch_tc_m<8, true>(p, L, grid, screen, st);
+    case 32: return launch_tc_m<16, false>(p, L, grid, screen, st);
+    case 33: return launch_tc_m<16, true>(p, L, grid, screen, st);
+    case 64: return launch_tc_m<32, false>(p, L, grid, screen, st);
+    case 65: return launch_tc_m<32, true>(p, L, grid, screen, st);
     }
     return cudaErrorInvalidValue;
 }
@@ -788,8 +851,11 @@ cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, c
 //   meta j: {H (fp32, rounded down), c_j bits, |c'|^2 rounded up, prefix max of that}
 //   columns past the k-1 neighbours: q = xx + 1e30 (never a winner), meta {NaN, c, 0, prefix}
 __global__ void k_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
-                          float *Bop, float4 *Bmeta)
+                          float *Bop, float4 *Bmeta, int16_t *rank)
 {
+    if (rank)   // rank[c][c'] = position of c' in c's neighbour list (the screen epilogue's own column)
+        for (int j = threadIdx.x; j < k - 1; j += blockDim.x)
+            rank[(int64_t)blockIdx.x * k + key_c(NL[(int64_t)blockIdx.x * ks + j])] = (int16_t)j;
     const int nmeta = tc_nmeta(nmax);
     extern __shared__ float4 smeta[];
     const int c = blockIdx.x, KT = tc_kt(DP);
@@ -833,9 +899,9 @@ __global__ void k_prep_tc(const double *C, const uint64_t *NL, int k, int d, int
 }
 
 cudaError_t launch_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
-                           float *Bop, float4 *Bmeta, cudaStream_t st)
+                           float *Bop, float4 *Bmeta, int16_t *rank, cudaStream_t st)
 {
-    k_prep_tc<<<k, 128, (size_t)tc_nmeta(nmax) * sizeof(float4), st>>>(C, NL, k, d, DP, ks, nmax, Bop, Bmeta);
+    k_prep_tc<<<k, 128, (size_t)tc_nmeta(nmax) * sizeof(float4), st>>>(C, NL, k, d, DP, ks, nmax, Bop, Bmeta, rank);
     return cudaGetLastError();
 }
 

@@ -47,6 +47,7 @@ KM_WALK_NAME(AssignParams p)
     const int n = (int)p.n;                        // < 2^31 (kmeans_create enforces it)
     const int kp = p.wpad;                          // candidate rows per cluster block
     const int kcols = k - 1;
+    constexpr int kChunk = kWalkChunk >= 2 * 32 * R ? kWalkChunk : 2 * 32 * R;   // rows per work claim (a multiple of 32 R)
     const int ib = p.wbits;                         // key index bits
     const uint32_t kmask = ~((1u << ib) - 1u);
     const float qtrunc = 1.f + __uint_as_float((uint32_t)(127 - 23 + ib) << 23) * 1.0001f;   // 1 + 2^(ib-23)
@@ -63,7 +64,7 @@ KM_WALK_NAME(AssignParams p)
         int c = 0;
         if (lane == 0) c = atomicAdd(p.work, 1);
         c = __shfl_sync(kFull, c, 0);
-        return c < (n + kWalkChunk - 1) / kWalkChunk ? c * kWalkChunk : n;   // n: no more work
+        return c < (n + kChunk - 1) / kChunk ? c * kChunk : n;   // n: no more work
     };
 #if KM_SKIP1
     // batch starts b0 (processed), b1 (rows staged), b2 (a/u staged); slot: the a/u slot of b0
@@ -73,7 +74,7 @@ KM_WALK_NAME(AssignParams p)
             const int c = claim();
             if (c >= n) { sk_next = sk_end = n; return n; }
             sk_next = c;
-            sk_end = min(c + kWalkChunk, n);
+            sk_end = min(c + kChunk, n);
         }
         const int b = sk_next;
         sk_next += kRows;
@@ -83,8 +84,11 @@ KM_WALK_NAME(AssignParams p)
     auto stage_au = [&](int r0, int sl) {          // a, u of rows [r0, r0 + 32 R) -> slot sl
         if (r0 < n) {
             float *ad = au_slot(sl);
-            if (lane < kRowsB / 4) cp_async16(ad + 4 * lane, p.a + r0 + 4 * lane);
-            else if (lane < kRowsB / 2) cp_async16(ad + kRowsB + 4 * (lane - kRowsB / 4), p.u + r0 + 4 * (lane - kRowsB / 4));
+#pragma unroll
+            for (int c = lane; c < kRowsB / 2; c += 32) {
+                if (c < kRowsB / 4) cp_async16(ad + 4 * c, p.a + r0 + 4 * c);
+                else cp_async16(ad + kRowsB + 4 * (c - kRowsB / 4), p.u + r0 + 4 * (c - kRowsB / 4));
+            }
         }
     };
     // x of the rows of batch r0 that fail clause 1 (their a/u are in slot sl): clause-1 rows are
@@ -92,27 +96,32 @@ KM_WALK_NAME(AssignParams p)
     auto stage_x_live = [&](int r0, int sl) {
         if (r0 >= n) return;
         const float *ad = au_slot(sl);
-        unsigned long long live = 0;
+        unsigned live[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const int r = 32 * i + lane;
             const int av = __float_as_int(ad[r]);
             const bool v = r0 + r < n;
             const bool l = v && !(__fadd_ru(ad[kRowsB + r], sF[v ? av : 0]) <= sS[v ? av : 0]);
-            live |= (unsigned long long)__ballot_sync(kFull, l) << (32 * i);
+            live[i] = __ballot_sync(kFull, l);
         }
         const float4 *xs = reinterpret_cast<const float4 *>(p.X + (size_t)r0 * DP);
         float4 *xd = reinterpret_cast<float4 *>(stg);
 #pragma unroll
-        for (int c = lane; c < kRowsB * DP / 4; c += 32)
-            if ((live >> (c / (DP / 4))) & 1ull) cp_async16(xd + stg_swz<DP>(c), xs + c);
+        for (int c = lane; c < kRowsB * DP / 4; c += 32) {
+            const int r = c / (DP / 4);
+            unsigned w = live[0];
+#pragma unroll
+            for (int i = 1; i < R; ++i) w = (r >> 5) == i ? live[i] : w;
+            if ((w >> (r & 31)) & 1u) cp_async16(xd + stg_swz<DP>(c), xs + c);
+        }
     };
     int chunk_row = n;
 #else
     // the work counter is fetched one chunk ahead by lane 0 and broadcast only when that chunk
     // starts, so the atomic's round trip overlaps a whole chunk of work
-    constexpr int kBatches = kWalkChunk / kRows;
-    const int nchunks = (n + kWalkChunk - 1) / kWalkChunk;
+    constexpr int kBatches = kChunk / kRows;
+    const int nchunks = (n + kChunk - 1) / kChunk;
     int chunk_row = claim();
     int ahead_c = 0;                                // lane 0: the claimed chunk after chunk_row
     if (lane == 0) ahead_c = atomicAdd(p.work, 1);
@@ -125,8 +134,11 @@ KM_WALK_NAME(AssignParams p)
 #pragma unroll
         for (int c = lane; c < kRowsB * DP / 4; c += 32) cp_async16(xd + stg_swz<DP>(c), xs + c);
         float *ad = stg + kRowsB * DP;
-        if (lane < kRowsB / 4) cp_async16(ad + 4 * lane, p.a + r0 + 4 * lane);
-        else if (lane < kRowsB / 2) cp_async16(ad + kRowsB + 4 * (lane - kRowsB / 4), p.u + r0 + 4 * (lane - kRowsB / 4));
+#pragma unroll
+        for (int c = lane; c < kRowsB / 2; c += 32) {
+            if (c < kRowsB / 4) cp_async16(ad + 4 * c, p.a + r0 + 4 * c);
+            else cp_async16(ad + kRowsB + 4 * (c - kRowsB / 4), p.u + r0 + 4 * (c - kRowsB / 4));
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #if KM_SKIP1
@@ -256,7 +268,7 @@ KM_WALK_NAME(AssignParams p)
         if (++bt == kBatches || chunk_row + bt * kRows >= n) {
             bt = 0;
             const int c = __shfl_sync(kFull, ahead_c, 0);
-            chunk_row = c < nchunks ? c * kWalkChunk : n;
+            chunk_row = c < nchunks ? c * kChunk : n;
             if (lane == 0 && chunk_row < n) ahead_c = atomicAdd(p.work, 1);
         }
         if (chunk_row < n) stage(chunk_row + bt * kRows);
@@ -269,13 +281,30 @@ KM_WALK_NAME(AssignParams p)
         for (int i = 0; i < R; ++i) { anew[i] = aold[i]; unew[i] = uu[i]; ut[i] = 0.f; defer[i] = false; }
         if (amask) {
             // warp cluster A: the middle row's if active, else the first active row's
-            const int mid = R == 1 ? 16 : 0;            // R = 2: lane 0 of the second half
-            const unsigned m_mid = __ballot_sync(kFull, active[R - 1]);
             int A;
-            if ((m_mid >> mid) & 1u) A = __shfl_sync(kFull, aold[R - 1], mid);
-            else {
-                const unsigned m0 = __ballot_sync(kFull, active[0]);
-                A = m0 ? __shfl_sync(kFull, aold[0], __ffs(m0) - 1) : __shfl_sync(kFull, aold[R - 1], __ffs(m_mid) - 1);
+            if constexpr (R <= 2) {
+                const int mid = R == 1 ? 16 : 0;            // R = 2: lane 0 of the second half
+                const unsigned m_mid = __ballot_sync(kFull, active[R - 1]);
+                if ((m_mid >> mid) & 1u) A = __shfl_sync(kFull, aold[R - 1], mid);
+                else {
+                    const unsigned m0 = __ballot_sync(kFull, active[0]);
+                    A = m0 ? __shfl_sync(kFull, aold[0], __ffs(m0) - 1) : __shfl_sync(kFull, aold[R - 1], __ffs(m_mid) - 1);
+                }
+            } else {                                       // row 32 (R / 2), else the first active row
+                const unsigned m_mid = __ballot_sync(kFull, active[R / 2]);
+                if (m_mid & 1u) A = __shfl_sync(kFull, aold[R / 2], 0);
+                else {
+                    int fi = 0, fl = 0;
+#pragma unroll
+                    for (int i = R - 1; i >= 0; --i) {
+                        const unsigned m = __ballot_sync(kFull, active[i]);
+                        if (m) { fi = i; fl = __ffs(m) - 1; }
+                    }
+                    int av = aold[0];
+#pragma unroll
+                    for (int i = 1; i < R; ++i) av = fi == i ? aold[i] : av;
+                    A = __shfl_sync(kFull, av, fl);
+                }
             }
             float4 cA[DP / 4];
 #pragma unroll

@@ -79,7 +79,8 @@ class KMeans:
                            "always": C.KM_RESORT_ALWAYS}[resort]
         o.resort_fraction = resort_fraction
         o.engine = {"auto": C.KM_ENGINE_AUTO, "cuda": C.KM_ENGINE_CUDA_CORE,
-                    "tensor": C.KM_ENGINE_TENSOR}[engine]
+                    "tensor": C.KM_ENGINE_TENSOR, "screen": C.KM_ENGINE_SCREEN,
+                    "tensor_screen": C.KM_ENGINE_TENSOR_SCREEN}[engine]
         o.spherical = int(bool(spherical))
         o.no_graph = int(not graph)
         o.force_comm = int(bool(force_comm))

@@ -49,8 +49,9 @@ def _independent_checks(X, a, u, Cused, rng, m):
     assert not bad.any(), int(bad.sum())
 
 
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
 @pytest.mark.parametrize("name", ["c3", "c4", "c5"])
-def test_full_size_trajectory(name):
+def test_full_size_trajectory(name, engine):
     path = os.path.join(GOLD, f"traj_{name}.json")
     if not os.path.exists(path):
         pytest.fail(f"missing golden trajectory {path} (tools/make_golden.py {name})")
@@ -62,8 +63,8 @@ def test_full_size_trajectory(name):
     assert X.shape == (spec.n, spec.d)
     assert sha256_points(X) == g["sha256_X"], "synthetic input differs from the golden run's"
     C0 = X[idx].astype(np.float64)
-    km = KMeans(torch.from_numpy(X).cuda(), C0, prune="mti")
-    assert km.engine == "k_walk"
+    km = KMeans(torch.from_numpy(X).cuda(), C0, prune="mti", engine=engine)
+    assert km.engine == {"cuda": "k_walk", "screen": "k_screen", "tensor_screen": "k_mti_tc_screen"}[engine]
     rng = np.random.default_rng(101)
     T = g["iterations"]
     check_at = {2, T}

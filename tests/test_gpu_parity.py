@@ -92,7 +92,7 @@ def test_B3_half_factor_on_gpu():
 
 
 # ---- seeded configs, free-running (strict tier) -------------------------------------------
-@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("none", "auto")])
+@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("mti", "screen"), ("mti", "tensor_screen"), ("none", "auto")])
 def test_c1_free_running(prune, engine):
     X, idx, _ = make_config("c1")
     C0 = X[idx].astype(float)
@@ -107,7 +107,7 @@ def test_c1_free_running(prune, engine):
         assert np.all(np.abs(gc - r.clause1) <= 1e-3 * 10000 + 1)
 
 
-@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("none", "auto")])
+@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("mti", "screen"), ("mti", "tensor_screen"), ("none", "auto")])
 def test_c2_free_running(prune, engine):
     X, idx, _ = make_config("c2")
     C0 = X[idx].astype(float)
@@ -119,7 +119,7 @@ def test_c2_free_running(prune, engine):
         assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
-@pytest.mark.parametrize("engine", ["tensor", "cuda"])
+@pytest.mark.parametrize("engine", ["tensor", "cuda", "screen", "tensor_screen"])
 @pytest.mark.parametrize("name,n,iters", [("c3", 2_000_000, 30), ("c4", 1_000_000, 30)])
 def test_spectral_shaped_free_running(name, n, iters, engine):
     X, idx, _ = make_config(name, n=n)
@@ -131,7 +131,7 @@ def test_spectral_shaped_free_running(name, n, iters, engine):
     assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
-@pytest.mark.parametrize("engine", ["tensor", "cuda"])
+@pytest.mark.parametrize("engine", ["tensor", "cuda", "screen", "tensor_screen"])
 def test_c5_shaped_large_k(engine):
     X, idx, _ = make_config("c5", n=300_000)
     C0 = X[idx].astype(float)
@@ -165,24 +165,26 @@ def test_c2_lockstep_single_step():
 
 
 # ---- edge cases ------------------------------------------------------------------------------
+@pytest.mark.parametrize("engine", ["cuda", "screen"])
 @pytest.mark.parametrize("d", [1, 2, 3, 5, 12, 33, 64])
-def test_dims_padding(d):
+def test_dims_padding(d, engine):
     rng = np.random.default_rng(d)
     X = (rng.normal(size=(3001, d)) + rng.integers(0, 4, size=(3001, 1)) * 3).astype(np.float32)
     C0 = X[rng.choice(3001, 7, replace=False)].astype(float)
     r = oracle.lloyd(X, C0, 60, 0, "brute")
     for prune in ("mti", "none"):
-        assert_strict(gpu_run(X, C0, 60, prune), r)
+        assert_strict(gpu_run(X, C0, 60, prune, engine=engine), r)
 
 
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
 @pytest.mark.parametrize("n", [1, 5, 31, 33, 257, 1000])
-def test_small_and_ragged_n(n):
+def test_small_and_ragged_n(n, engine):
     rng = np.random.default_rng(n)
-    X = rng.normal(size=(n, 4)).astype(np.float32)
+    X = rng.normal(size=(n, 8 if engine == "tensor_screen" else 4)).astype(np.float32)   # tcgen05: d padded to 8/16/32
     k = min(n, 3)
     C0 = X[:k].astype(float)
     r = oracle.lloyd(X, C0, 30, 0, "brute")
-    assert_strict(gpu_run(X, C0, 30, "mti"), r)
+    assert_strict(gpu_run(X, C0, 30, "mti", engine=engine), r)
 
 
 def test_k1_and_k_equals_n():
@@ -199,12 +201,13 @@ def test_k1_and_k_equals_n():
     assert g["sse"] == 0.0
 
 
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
 @pytest.mark.parametrize("policy", ["never", "always", "auto"])
-def test_resort_policies_agree(policy):
+def test_resort_policies_agree(policy, engine):
     X, idx, _ = make_config("c3", n=400_000)
     C0 = X[idx].astype(float)
     r = oracle.lloyd(X, C0, 12, 0, "mti")
-    assert_strict(gpu_run(X, C0, 12, "mti", resort=policy), r)
+    assert_strict(gpu_run(X, C0, 12, "mti", resort=policy, engine=engine), r)
 
 
 def test_max_iters_zero_and_host_points():
@@ -238,14 +241,15 @@ def test_usage_errors():
         KMeans(np.ones((10, 2), np.float32), np.array([[0, np.inf], [1, 1]]), check_finite=True)
 
 
-def test_bound_soundness_sampled():
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
+def test_bound_soundness_sampled(engine):
     """u_i >= ||x_i - C_used[a_i]|| (fp64, against the fp64 centroids the pass used) for every row
     after every pass, read through kmeans_get_bounds (u loosened by drift,
     tightened by U(u)); assignments equal the fp64 brute-force argmin of C_used."""
     X, idx, _ = make_config("c2")
     C0 = X[idx].astype(float)
     Xd = torch.from_numpy(X).cuda()
-    km = KMeans(Xd, C0, prune="mti")
+    km = KMeans(Xd, C0, prune="mti", engine=engine)
     with pytest.raises(KMeansError, match="KM_ESTATE"):
         km.bounds()
     for _ in range(8):
