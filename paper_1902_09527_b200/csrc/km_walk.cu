@@ -96,10 +96,10 @@ cudaError_t launch_prep_walk(const double *C, const uint64_t *NL, int k, int d, 
 
 size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem, bool skip1)
 {
-    const int R = DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1);
+    const int R = walk_r_sel(DP, wh_smem);
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
-           (size_t)(walk_threads_rt(DP) / 32) * walk_warp_floats(DP, R, skip1 ? 1 : 0) * sizeof(float);
+           (size_t)(walk_threads_dr(DP, R) / 32) * walk_warp_floats(DP, R, skip1 ? 1 : 0) * sizeof(float);
 }
 
 
@@ -116,11 +116,11 @@ typedef void (*walk_kernel_t)(AssignParams);
         }                                                                            \
     } else {                                                                         \
         switch (whs) {                                                               \
-        case 256: return K<DP, CSMEM, R, 256, false>;                                \
-        case 512: return K<DP, CSMEM, R, 512, false>;                                \
-        case 1024: return K<DP, CSMEM, R, 1024, false>;                              \
-        case 2048: return K<DP, CSMEM, R, 2048, false>;                              \
-        case 4096: return K<DP, CSMEM, R, 4096, false>;                              \
+        case 256: return K<DP, CSMEM, RG, 256, false>;                               \
+        case 512: return K<DP, CSMEM, RG, 512, false>;                               \
+        case 1024: return K<DP, CSMEM, RG, 1024, false>;                             \
+        case 2048: return K<DP, CSMEM, RG, 2048, false>;                             \
+        case 4096: return K<DP, CSMEM, RG, 4096, false>;                             \
         }                                                                            \
     }                                                                                \
     return nullptr;
@@ -129,6 +129,7 @@ template <int DP, bool CSMEM, bool SK>
 static walk_kernel_t walk_pick_s(int whs, bool hs)
 {
     constexpr int R = walk_r<DP>();
+    constexpr int RG = DP == 32 ? KM_WALK_R32G : R;   // rows per lane when the H rows are global
     if constexpr (SK) {
         KM_WALK_PICK(k_walk_skip1)
     } else {
@@ -170,7 +171,7 @@ cudaError_t launch_walk(int DP, bool csmem, const AssignParams &p, int grid, boo
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, walk_threads_rt(DP), sm, st>>>(p);
+    kern<<<grid, walk_threads_dr(DP, walk_r_sel(DP, p.wh_smem != 0)), sm, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -183,7 +184,7 @@ int walk_grid(int DP, bool csmem, int k, int whs, bool hs, int num_sms)
         const size_t sm = walk_smem(DP, csmem, k, whs, hs, sk != 0);
         if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, walk_threads_rt(DP), sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, walk_threads_dr(DP, walk_r_sel(DP, hs)), sm);
         per_sm = per_sm < 1 ? 1 : per_sm;
         best = sk == 0 ? per_sm : std::min(best, per_sm);
     }

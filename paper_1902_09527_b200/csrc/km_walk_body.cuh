@@ -6,7 +6,7 @@
 // A preprocessor switch (not a template parameter) keeps the KM_SKIP1 0 kernel's source, and so
 // its register allocation, exactly the measured k_walk's.
 template <int DP, bool CSMEM, int R, int NH, bool HSMEM>
-__global__ void __launch_bounds__(walk_threads<DP>(), 1)
+__global__ void __launch_bounds__(walk_threads_dr(DP, R), 1)
 KM_WALK_NAME(AssignParams p)
 {
     extern __shared__ __align__(16) float smem[];

@@ -148,6 +148,21 @@ template <int DP> constexpr int walk_threads() { return walk_threads_of(DP); }
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
 template <int DP> constexpr int walk_r() { return DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1); }
 static inline int walk_r_rt(int DP) { return DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1); }
+// d = 32 with the H rows in global memory (large k, C5): three rows per lane at 256 threads per
+// CTA — each candidate pair block a warp loads (256 B, delivered to all 32 lanes through the L1
+// data pipe) then serves 96 rows; measured on C5: 28.0 -> 24.4 ms per pass; on C4 (H rows in
+// shared memory) two rows at 384 threads stay faster (6.27 vs 7.60 ms)
+#ifndef KM_WALK_R32G
+#define KM_WALK_R32G 3
+#endif
+#ifndef KM_WALK_T32G
+#define KM_WALK_T32G 256
+#endif
+__host__ __device__ constexpr int walk_threads_dr(int DP, int R)
+{
+    return (DP == 32 && R == KM_WALK_R32G && R != KM_WALK_R32) ? KM_WALK_T32G : walk_threads_of(DP);
+}
+static inline int walk_r_sel(int DP, bool hs) { return (DP == 32 && !hs) ? KM_WALK_R32G : walk_r_rt(DP); }
 static inline int walk_threads_rt(int DP) { return walk_threads_of(DP); }
 
 // Staged row r, 16-byte part q (of DP/4) lives in float4 slot r (DP/4) + (q ^ g(r)): the lanes of
