@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats-out", default=None)
-    ap.add_argument("--engine", default="auto", choices=["auto", "cuda", "tensor", "screen", "tensor_screen"],
+    ap.add_argument("--engine", default="auto", choices=["auto", "cuda", "tensor", "screen", "tensor_screen", "tensor_chunked"],
                     help="MTI pass engine (auto = the CUDA-core walk k_walk)")
     ap.add_argument("--resort-fraction", type=float, default=0.0)
     ap.add_argument("--no-graph", action="store_true", help="launch each iteration eagerly (no CUDA graph)")

@@ -65,10 +65,12 @@ enum { KM_RESORT_AUTO = 0, KM_RESORT_NEVER = 1, KM_RESORT_ALWAYS = 2 };
  * rows that provably stay are decided; "k_resolve": the queued rest, direct form + exact-mode
  * decision).  TENSOR: the tcgen05 TF32x3 kernel ("k_mti_tc"; d padded to 8, 16 or 32; measured
  * slower, opt-in).  TENSOR_SCREEN: the tcgen05 kernel screening (smallest column value only, rows
- * that provably stay decided; "k_mti_tc_screen") followed by k_resolve.  All give the same (exact-mode) assignments.  Iteration 1 and KM_PRUNE_NONE
+ * that provably stay decided; "k_mti_tc_screen") followed by k_resolve.  TENSOR_CHUNKED: the
+ * tcgen05 screen over the whole neighbour list in 128-column chunks ("k_tcc", km_tcc.cu; no
+ * column cap, for large k) followed by k_resolve.  All give the same (exact-mode) assignments.  Iteration 1 and KM_PRUNE_NONE
  * always use the CUDA-core dense kernel. */
 enum { KM_ENGINE_AUTO = 0, KM_ENGINE_CUDA_CORE = 1, KM_ENGINE_TENSOR = 2, KM_ENGINE_SCREEN = 3,
-       KM_ENGINE_TENSOR_SCREEN = 4 };
+       KM_ENGINE_TENSOR_SCREEN = 4, KM_ENGINE_TENSOR_CHUNKED = 5 };
 
 typedef struct km_options {
     int32_t device;            /* CUDA device ordinal the context lives on */

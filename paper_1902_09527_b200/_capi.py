@@ -16,7 +16,7 @@ SO_PATH = os.environ.get("KM_LIB") or os.path.join(_PKG, "libkmeans_b200.so")
 KM_OK, KM_EARG, KM_ENONFINITE, KM_ECUDA, KM_ENCCL, KM_ENOMEM, KM_ESTATE = range(7)
 KM_PRUNE_MTI, KM_PRUNE_NONE, KM_PRUNE_TI = 0, 1, 2
 KM_RESORT_AUTO, KM_RESORT_NEVER, KM_RESORT_ALWAYS = 0, 1, 2
-KM_ENGINE_AUTO, KM_ENGINE_CUDA_CORE, KM_ENGINE_TENSOR, KM_ENGINE_SCREEN, KM_ENGINE_TENSOR_SCREEN = 0, 1, 2, 3, 4
+KM_ENGINE_AUTO, KM_ENGINE_CUDA_CORE, KM_ENGINE_TENSOR, KM_ENGINE_SCREEN, KM_ENGINE_TENSOR_SCREEN, KM_ENGINE_TENSOR_CHUNKED = 0, 1, 2, 3, 4, 5
 STATUS_NAMES = {0: "KM_OK", 1: "KM_EARG", 2: "KM_ENONFINITE", 3: "KM_ECUDA", 4: "KM_ENCCL",
                 5: "KM_ENOMEM", 6: "KM_ESTATE"}
 

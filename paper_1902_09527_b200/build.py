@@ -13,8 +13,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SO = os.path.join(PKG, "libkmeans_b200.so")
-SRCS = [os.path.join(PKG, "csrc", f) for f in ("km_kernels.cu", "km_tc.cu", "km_walk.cu", "km_screen.cu", "km_ti.cu", "km_seed.cu", "km_api.cu")]
-DEPS = SRCS + [os.path.join(PKG, "csrc", "km_device.cuh"), os.path.join(PKG, "csrc", "km_walk_body.cuh"), os.path.join(PKG, "csrc", "km_walk_common.cuh"), os.path.join(PKG, "csrc", "km_kernels.cuh"), os.path.join(ROOT, "include", "kmeans_b200.h")]
+SRCS = [os.path.join(PKG, "csrc", f) for f in ("km_kernels.cu", "km_tc.cu", "km_walk.cu", "km_screen.cu", "km_tcc.cu", "km_ti.cu", "km_seed.cu", "km_api.cu")]
+DEPS = SRCS + [os.path.join(PKG, "csrc", "km_device.cuh"), os.path.join(PKG, "csrc", "km_walk_body.cuh"), os.path.join(PKG, "csrc", "km_walk_common.cuh"), os.path.join(PKG, "csrc", "km_tc_common.cuh"), os.path.join(PKG, "csrc", "km_kernels.cuh"), os.path.join(ROOT, "include", "kmeans_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

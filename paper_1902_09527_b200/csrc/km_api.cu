@@ -204,6 +204,11 @@ struct km_ctx {
     bool use_screen = false;        // CUDA-core screen (k_screen) or, with use_tc, tensor screen
     int *qrow = nullptr, *qcnt = nullptr;   // per 32-row group: queued rows, count
     int16_t *nlrank = nullptr;      // tensor screen: k x k neighbour-list positions
+    // column-chunked tensor-core screen (km_tcc.cu)
+    bool use_tcc = false;
+    float *Bc = nullptr;
+    float2 *Mc = nullptr;
+    int tcc_nch = 0, tcc_nmeta = 0;
     int screen_grid = 0, resolve_grid = 0;
     int64_t launches = 0;
 };
@@ -234,6 +239,11 @@ km_status prep(km_ctx *c)
     }
     if (c->use_ti) {
         KM_CUDA(km::launch_prep_ti(c->NL, c->k, c->ks, c->Hm, c->st));
+        c->launches += 1;
+    }
+    if (c->use_tcc) {
+        KM_CUDA(km::launch_prep_tcc(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->tcc_nch, c->tcc_nmeta, c->Bc, c->Mc,
+                                    c->nlrank, c->st));
         c->launches += 1;
     }
     if (c->use_tc) {
@@ -286,6 +296,9 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
     p.qrow = c->qrow;
     p.qcnt = c->qcnt;
     p.rank = c->nlrank;
+    p.Bc = c->Bc;
+    p.Mc = c->Mc;
+    p.tcc_nch = c->tcc_nch;
     return p;
 }
 
@@ -294,6 +307,10 @@ km_status launch_assign(km_ctx *c, int mode, int work_slot)
     km::AssignParams p = assign_params(c, work_slot);
     if (c->use_ti && (mode == km::MODE_MTI_REDUCE || mode == km::MODE_DENSE)) {
         KM_CUDA(km::launch_ti(c->DP, c->csmem, mode == km::MODE_DENSE, p, c->L, c->Hm, c->ti_grid, c->st));
+    } else if (mode == km::MODE_MTI_REDUCE && c->use_tcc) {
+        KM_CUDA(km::launch_tcc(c->DP, c->csmem, p, c->num_sms, c->st));
+        KM_CUDA(km::launch_resolve(c->DP, c->csmem, p, c->resolve_grid, c->st));
+        c->launches += 1;
     } else if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
         if (c->use_tc) {
             KM_CUDA(km::launch_mti_tc(c->DP, c->csmem, p, c->tc_grid, c->use_screen, c->st));
@@ -413,7 +430,7 @@ km_status enqueue_body(km_ctx *c, bool full = false)
     KM_CUDA(rec_event(ev[5], c->st));
     // the walk, tensor-core and TI passes reduce only the rows that moved (S += acc, reading B5);
     // the knori- and legacy passes reduce every row (S = acc)
-    const int delta = (c->use_walk || c->use_tc || c->use_ti) && !full ? 1 : 0;
+    const int delta = (c->use_walk || c->use_tc || c->use_tcc || c->use_ti) && !full ? 1 : 0;
     KM_CUDA(km::launch_update(c->acc, c->S, delta, c->C, c->Cprev, c->k, c->d, c->DP,
                               c->empty, c->spherical ? 1 : 0, c->st));
     c->launches += 1;
@@ -504,7 +521,7 @@ km_status iterate(km_ctx *c, int64_t *changed_out, int64_t *dists_out)
         KM_CUDA(cudaEventRecord(ev[6], c->st));
     } else {
         // the decision uses global counts only, so every rank takes it in the same iteration
-        const bool full = (c->use_walk || c->use_tc || c->use_ti) && c->resum_moves >= 0.0 &&
+        const bool full = (c->use_walk || c->use_tc || c->use_tcc || c->use_ti) && c->resum_moves >= 0.0 &&
                           (double)c->moves_since_full > c->resum_moves * (double)c->n_global;
         if (full) {
             KM_TRY(enqueue_body(c, true));
@@ -552,7 +569,7 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base); cudaFree(c->lohist); cudaFree(c->qmap);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P); cudaFree(c->qrow); cudaFree(c->qcnt); cudaFree(c->nlrank);
+    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P); cudaFree(c->qrow); cudaFree(c->qcnt); cudaFree(c->nlrank); cudaFree(c->Bc); cudaFree(c->Mc);
     cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part); cudaFree(c->L); cudaFree(c->Hm);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -700,6 +717,24 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     }
     // AUTO: the CUDA-core walk (measured faster than the tensor-core pipeline on C3 and C4 so
     // far); KM_ENGINE_TENSOR selects the tcgen05 kernel
+    // (k = 1 or another prune mode: the default engines, as for the walk)
+    if (o->engine == KM_ENGINE_TENSOR_CHUNKED && c->prune == KM_PRUNE_MTI && !c->use_ti && k >= 2) {
+        if (!km::tc_supported(DP))
+            return fail(KM_EARG, "tensor_chunked engine needs d padded to 8, 16 or 32 (d=%d)", d);
+        if (km::tcc_smem(DP, c->csmem, k) == 0)
+            return fail(KM_EARG, "tensor_chunked engine: shared memory for d=%d k=%d exceeds one SM", d, k);
+        c->use_tcc = true;
+        c->use_screen = true;
+        c->tcc_nch = km::tcc_nch_host(k);
+        c->tcc_nmeta = km::tcc_nmeta_host(k);
+        KM_TRY(dalloc(&c->Bc, (size_t)k * c->tcc_nch * 128 * km::tcc_ka_host(DP)));
+        KM_TRY(dalloc(&c->Mc, (size_t)k * c->tcc_nmeta));
+        KM_TRY(dalloc(&c->nlrank, (size_t)k * k));
+        KM_TRY(dalloc(&c->qrow, (size_t)c->n_alloc));
+        KM_TRY(dalloc(&c->qcnt, (size_t)(c->n_alloc / 32)));
+        c->resolve_grid = km::resolve_grid(DP, c->csmem, k, c->num_sms);
+        c->part_grid = std::max(c->part_grid, std::max(c->resolve_grid, c->num_sms));
+    }
     const bool want_tc = o->engine == KM_ENGINE_TENSOR || o->engine == KM_ENGINE_TENSOR_SCREEN;
     c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 && !c->use_ti && want_tc;
     if (want_tc && !km::tc_supported(DP))
@@ -743,7 +778,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
 #ifdef KM_LEGACY_WALK
     c->use_walk = false;
 #else
-    c->use_walk = !c->use_tc && !c->use_ti && c->prune == KM_PRUNE_MTI && k >= 2 && km::walk_supported(DP);
+    c->use_walk = !c->use_tc && !c->use_tcc && !c->use_ti && c->prune == KM_PRUNE_MTI && k >= 2 && km::walk_supported(DP);
 #endif
     if (c->use_walk) {
         c->wpad = (k + 1) & ~1;                    // k-1 neighbours + >= 1 dummy row, even
@@ -774,7 +809,7 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
     }
     // engines that handle rows outside the warp's / tile's cluster by the triangle bound only
     // re-bucket when the layout is badly mixed
-    if ((c->use_tc || c->use_walk) && !(o->resort_fraction > 0.f)) c->resort_fraction = 0.25f;
+    if ((c->use_tc || c->use_tcc || c->use_walk) && !(o->resort_fraction > 0.f)) c->resort_fraction = 0.25f;
     c->nslab = std::min(c->part_grid, c->num_sms);
     KM_TRY(dalloc(&c->acc_part, (size_t)c->nslab * k * (DP + 1)));
     c->use_graph = o->no_graph == 0;
@@ -998,6 +1033,7 @@ const char *kmeans_engine(const km_ctx *c)
     if (!c) return "";
     if (c->prune == KM_PRUNE_NONE) return "k_assign_dense";
     if (c->use_ti) return "k_ti";
+    if (c->use_tcc) return "k_tcc";
     if (c->use_tc && c->use_screen) return "k_mti_tc_screen";
     return c->use_tc ? "k_mti_tc" : (c->use_walk ? (c->use_screen ? "k_screen" : "k_walk") : "k_assign");
 }

@@ -75,6 +75,10 @@ struct AssignParams {
     int *qrow;
     int *qcnt;
     const int16_t *rank;   // k x k: position of c' in c's neighbour list (tensor-screen epilogue)
+    // column-chunked tensor-core screen (k_tcc, km_tcc.cu)
+    const float *Bc;       // k x tcc_nch x (128 x (2 DP + 8)): B operand chunks (UMMA K-major)
+    const float2 *Mc;      // k x nmeta: {H, prefix max of |c'|^2 (up)}
+    int32_t tcc_nch;       // chunks per cluster list
 };
 
 struct PrepParams {
@@ -119,6 +123,13 @@ cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, b
 cudaError_t launch_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
                            float *Bop, float4 *Bmeta, int16_t *rank, cudaStream_t st);
 cudaError_t launch_resolve(int DP, bool csmem, const AssignParams &p, int g_resolve, cudaStream_t st);
+cudaError_t launch_tcc(int DP, bool csmem, const AssignParams &p, int num_sms, cudaStream_t st);
+cudaError_t launch_prep_tcc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nch, int nmeta,
+                            float *Bc, float2 *Mc, int16_t *rank, cudaStream_t st);
+size_t tcc_smem(int DP, bool csmem, int k);
+int tcc_nch_host(int k);
+int tcc_ka_host(int DP);
+int tcc_nmeta_host(int k);
 int resolve_grid(int DP, bool csmem, int k, int num_sms);
 cudaError_t launch_mti_count(const unsigned long long *defer, const int *dcount, int64_t ntiles,
                              unsigned long long *counters, const uint64_t *NL, int ks, int k, int num_sms,

@@ -1,0 +1,578 @@
+// km_tcc.cu — column-chunked tensor-core MTI screen ("tensor-chunked" engine), sm_100a.
+//
+// Method: PAPER.md §3.3 (1026-1053): u += f(a), clause 1, tightening U(u), clauses 2/3 over the
+// neighbour list of the row's cluster (readings A1/A5/A6); the rows that provably stay are decided
+// here, the rest is queued for k_resolve (km_screen.cu), which takes the exact-mode decision and
+// applies the moves (reading B5).  DESIGN.md §10.
+//
+// Why.  The CUDA-core walk delivers every candidate row to every lane through the L1 data pipe
+// (256 B per candidate pair at d = 32), which bounds C5 — where a quarter of the active rows need
+// nearly all 999 candidates — at ~0.5 wavefront per row-candidate.  Here the candidates of a
+// 128-row tile (rows bucketed by cluster, the tile's cluster A = its middle row's) are evaluated
+// by tcgen05.mma reading both operands from shared memory, 128 columns at a time:
+//
+//   producer warp   TMA bulk copies of the row tiles [x | a | u] into a 2-stage ring
+//   4 prep warps    per row: u += f(a), clause 1, x' = x - C^[A], |x'|^2, the tightened bound
+//                   u_t (rows of another cluster: direct distance to their own centroid, columns
+//                   up to the triangle bound (u_t + d(x, A)) / 2), the prefix p = #{j : H[A][j] <
+//                   T}; the A operand row [x'hi | x'lo | |x'|^2 hi, lo, 1, 1, 0..] (TF32 split by
+//                   truncation, as the tensor core truncates)
+//   MMA warp        per 128-column chunk of A's list: a TMA bulk copy of the chunk's B operand
+//                   ([-2c'hi | -2c'lo | 1, 1, |c'|^2 hi, lo, 0..], c' = C^[c_j] - C^[A]) into a
+//                   2-slot ring, then x'hi.c'hi + x'lo.c'hi + x'hi.c'lo + extras as four MMA groups
+//                   sharing the operands (the TF32x3 products of k_mti_tc, K = 2 DP + 8 stored
+//                   instead of 3 DP + 8) into a 2-buffer TMEM ring
+//   4 epilogue warps per chunk: tcgen05.ld, the running minimum of each row's columns (the own
+//                   column masked for rows of another cluster); per tile: the row stays iff the
+//                   minimum exceeds (u_t + eps)^2 + E (the error model of k_mti_tc),
+//                   else it is queued
+//
+// Exactness is k_mti_tc's (the same products, the same bound κ); every row it cannot decide goes
+// to k_resolve.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "km_device.cuh"
+#include "km_kernels.cuh"
+#include "km_tc_common.cuh"
+
+namespace km {
+
+constexpr int kCRows = 128;            // rows per tile (MMA M)
+constexpr int kCNC = 128;              // columns per chunk (MMA N <= 128)
+constexpr int kCThreads = 320;
+constexpr int kCPrepW = 4;             // warps 0-3: prep
+constexpr int kCEpiW0 = 4;             // warps 4-7: epilogue (TMEM lane quadrant = warp % 4)
+constexpr int kCProdW = 8;             // warp 8: row-tile producer
+constexpr int kCMmaW = 9;              // warp 9: B-chunk loads + MMA issue
+constexpr int kCStages = 2;
+
+__host__ __device__ constexpr int tcc_ka(int DP) { return 2 * DP + 8; }
+
+struct TccRow {
+    int a;          // assignment before the pass
+    int flags;      // bit0 valid, bit1 active (clause 1 failed), bit2 misfit (a != A)
+    float uu;       // u + f(a)
+    float ut;       // tightened upper bound of d(x, C[a])
+    float xx;       // |x - C^[A]|^2
+    int p;          // columns below the row's threshold
+    int own;        // misfit: position of a in A's list, else -1
+    int pad;
+};
+
+struct TccInfo {
+    long long tile;  // -1 = end of stream
+    int A, N, nch;   // tile cluster, MMA columns (multiple of 16), chunks
+    int pw[4];       // per-warp columns the epilogue reads
+    float cm[4];     // per-warp prefix max of |c'|^2 over those columns
+};
+
+struct TccCfg {
+    int stage_bytes, ring, aop, bop, meta, rstate, sc, sf, ss, total;
+};
+
+__host__ __device__ inline TccCfg tcc_cfg(int DP, bool csmem, int k, int nmeta)
+{
+    TccCfg L;
+    const int KA = tcc_ka(DP);
+    L.stage_bytes = kCRows * DP * 4 + 2 * kCRows * 4;
+    L.ring = 0;
+    L.aop = (L.ring + kCStages * L.stage_bytes + 127) & ~127;
+    L.bop = L.aop + 2 * kCRows * KA * 4;
+    L.meta = L.bop + 2 * kCNC * KA * 4;
+    L.rstate = L.meta + 2 * nmeta * 8;
+    L.sc = L.rstate + 2 * kCRows * (int)sizeof(TccRow);
+    L.sf = L.sc + (csmem ? k * DP * 4 : 0);
+    L.ss = L.sf + ((k + 3) & ~3) * 4;
+    L.total = L.ss + ((k + 3) & ~3) * 4;
+    return L;
+}
+
+// #{j < M : meta[j].x < T} (ascending, NaN padded), M a power of two
+template <int M>
+__device__ __forceinline__ int count_below2(const float2 *meta, float T)
+{
+    int base = 0;
+#pragma unroll
+    for (int half = M >> 1; half >= 1; half >>= 1)
+        base = meta[base + half - 1].x < T ? base + half : base;
+    return base + (meta[base].x < T ? 1 : 0);
+}
+
+__device__ __forceinline__ float tcc_fmin3(float a, float b, float c)
+{
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+template <int DP, bool CSMEM, int NMETA>
+__global__ void __launch_bounds__(kCThreads, 1)
+k_tcc(AssignParams p, TccCfg L)
+{
+    constexpr int KA = tcc_ka(DP);
+    constexpr uint32_t kBBytes = kCNC * KA * 4;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t s_full[kCStages], s_sfree[kCStages];
+    __shared__ __align__(8) uint64_t s_aready[2], s_efree[2], s_bfull[2], s_bempty[2], s_tfull[2], s_tfree[2], s_mbar[2];
+    __shared__ long long s_meta[kCStages];
+    __shared__ TccInfo s_info[2];
+    __shared__ uint32_t s_tmem;
+
+    const int k = p.k;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t sbase = tc::smem_u32(smem);
+    float *sC = reinterpret_cast<float *>(smem + L.sc);
+    float *sF = reinterpret_cast<float *>(smem + L.sf);
+    float *sS = reinterpret_cast<float *>(smem + L.ss);
+    TccRow *rstate = reinterpret_cast<TccRow *>(smem + L.rstate);
+    const float2 *meta0 = reinterpret_cast<const float2 *>(smem + L.meta);
+
+    if (CSMEM) {
+        const float4 *src = reinterpret_cast<const float4 *>(p.Cneg);
+        float4 *dst = reinterpret_cast<float4 *>(sC);
+        for (int i = t; i < k * DP / 4; i += kCThreads) dst[i] = src[i];
+    }
+    for (int i = t; i < k; i += kCThreads) { sF[i] = p.f[i]; sS[i] = p.s[i]; }
+    {   // zero the A operand buffers once (rows of clause-1 threads are never written)
+        float4 *za = reinterpret_cast<float4 *>(smem + L.aop);
+        for (int i = t; i < 2 * kCRows * KA / 4; i += kCThreads) za[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (warp == kCMmaW) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(tc::smem_u32(&s_tmem)), "r"(2 * kCNC));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        for (int s = 0; s < kCStages; ++s) {
+            tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
+            tc::mbar_init(tc::smem_u32(&s_sfree[s]), kCPrepW);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(tc::smem_u32(&s_aready[b]), kCPrepW);
+            tc::mbar_init(tc::smem_u32(&s_efree[b]), 4);
+            tc::mbar_init(tc::smem_u32(&s_bfull[b]), 1);
+            tc::mbar_init(tc::smem_u32(&s_bempty[b]), 1);
+            tc::mbar_init(tc::smem_u32(&s_tfull[b]), 1);
+            tc::mbar_init(tc::smem_u32(&s_tfree[b]), 4);
+            tc::mbar_init(tc::smem_u32(&s_mbar[b]), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const int64_t n = p.n;
+    const int64_t ntiles = (n + kCRows - 1) / kCRows;
+
+    if (warp == kCProdW) {
+        // ================= producer: row tiles [x | a | u] -> ring stages ==================
+        if (lane == 0) {
+            const int G = p.tile_chunk;
+            int64_t q_next = 0, q_end = 0;
+            for (int L_ = 0;; ++L_) {
+                const int s = L_ % kCStages;
+                if (L_ >= kCStages) tc::mbar_wait(tc::smem_u32(&s_sfree[s]), (uint32_t)(((L_ / kCStages) - 1) & 1));
+                if (q_next >= q_end) {
+                    const int64_t c = atomicAdd(p.work, 1);
+                    q_next = c * G;
+                    q_end = q_next + G;
+                }
+                const int64_t tl = q_next < ntiles ? q_next : -1;
+                ++q_next;
+                s_meta[s] = tl;
+                const uint32_t mb = tc::smem_u32(&s_full[s]);
+                if (tl < 0) { tc::mbar_arrive(mb); break; }
+                const uint32_t xb = kCRows * DP * 4, ab = kCRows * 4;
+                tc::mbar_arrive_tx(mb, xb + 2 * ab);
+                const uint32_t dst = sbase + L.ring + s * L.stage_bytes;
+                tc::bulk_g2s(dst, p.X + tl * kCRows * DP, xb, mb);
+                tc::bulk_g2s(dst + xb, p.a + tl * kCRows, ab, mb);
+                tc::bulk_g2s(dst + xb + ab, p.u + tl * kCRows, ab, mb);
+            }
+        }
+    } else if (warp == kCMmaW) {
+        // ================= B chunks + MMA: D[chunk] = A . B[chunk]^T ========================
+        if (lane == 0) {
+            const uint32_t idesc_base = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCRows >> 4) << 24);
+            const uint32_t bfull[2] = {tc::smem_u32(&s_bfull[0]), tc::smem_u32(&s_bfull[1])};
+            const uint32_t bempty[2] = {tc::smem_u32(&s_bempty[0]), tc::smem_u32(&s_bempty[1])};
+            const uint32_t tfull[2] = {tc::smem_u32(&s_tfull[0]), tc::smem_u32(&s_tfull[1])};
+            const uint32_t tfree[2] = {tc::smem_u32(&s_tfree[0]), tc::smem_u32(&s_tfree[1])};
+            uint32_t g = 0;                               // chunks issued so far
+            for (int i = 0;; ++i) {
+                const int b = i & 1;
+                tc::mbar_wait(tc::smem_u32(&s_aready[b]), (uint32_t)((i >> 1) & 1));
+                tc::fence_after();
+                const TccInfo &inf = s_info[b];
+                if (inf.tile < 0) break;
+                const int A = inf.A, N = inf.N, nch = inf.nch;
+                const uint32_t ab = sbase + L.aop + (uint32_t)(b * kCRows * KA * 4);
+                const float *bsrc = p.Bc + (int64_t)A * p.tcc_nch * kCNC * KA;
+                auto load_b = [&](uint32_t gg, int ch) {  // chunk ch of A's list -> slot gg & 1
+                    const int j = gg & 1;
+                    if (gg >= 2) tc::mbar_wait(bempty[j], ((gg - 2) >> 1) & 1);
+                    tc::mbar_arrive_tx(bfull[j], kBBytes);
+                    tc::bulk_g2s(sbase + L.bop + j * kBBytes, bsrc + (int64_t)ch * kCNC * KA, kBBytes, bfull[j]);
+                };
+                if (nch > 0) load_b(g, 0);
+                for (int ch = 0; ch < nch; ++ch, ++g) {
+                    const int j = g & 1;
+                    if (ch + 1 < nch) load_b(g + 1, ch + 1);   // next chunk's copy overlaps these MMAs
+                    tc::mbar_wait(bfull[j], (g >> 1) & 1);
+                    if (g >= 2) tc::mbar_wait(tfree[j], ((g - 2) >> 1) & 1);
+                    tc::fence_after();
+                    const int w = min(kCNC, N - ch * kCNC);
+                    const uint32_t idesc = idesc_base | ((uint32_t)(w >> 3) << 17);
+                    const uint32_t bb = sbase + L.bop + j * kBBytes;
+                    const uint32_t d = s_tmem + (uint32_t)(j * kCNC);
+#pragma unroll
+                    for (int kb = 0; kb < DP / 8; ++kb)       // x'hi . c'hi
+                        tc::mma_tf32(d, tc::sdesc(ab + kb * kCRows * 32), tc::sdesc(bb + kb * kCNC * 32), idesc, kb > 0);
+#pragma unroll
+                    for (int kb = 0; kb < DP / 8; ++kb)       // x'lo . c'hi
+                        tc::mma_tf32(d, tc::sdesc(ab + (DP / 8 + kb) * kCRows * 32), tc::sdesc(bb + kb * kCNC * 32), idesc, 1);
+#pragma unroll
+                    for (int kb = 0; kb < DP / 8; ++kb)       // x'hi . c'lo
+                        tc::mma_tf32(d, tc::sdesc(ab + kb * kCRows * 32), tc::sdesc(bb + (DP / 8 + kb) * kCNC * 32), idesc, 1);
+                    tc::mma_tf32(d, tc::sdesc(ab + (DP / 4) * kCRows * 32), tc::sdesc(bb + (DP / 4) * kCNC * 32), idesc, 1);
+                    tc::mma_commit(tfull[j]);
+                    tc::mma_commit(bempty[j]);
+                }
+            }
+        }
+    } else if (warp < kCPrepW) {
+        // ================= prep: bounds, clause 1, tightening, prefix, A operand ============
+        const float eps = *p.eps;
+        const int ncols = k - 1;
+        CRow<CSMEM> Cn;
+        if constexpr (CSMEM) Cn.base = tc::smem_u32(sC); else Cn.base = p.Cneg;
+        int mA[2] = {-1, -1};
+        uint32_t mpar[2] = {0u, 0u};
+        int mcur = 0;
+        unsigned long long c_clause1 = 0;
+        for (int i = 0;; ++i) {
+            const int s = i % kCStages, b = i & 1;
+            tc::mbar_wait(tc::smem_u32(&s_full[s]), (uint32_t)((i / kCStages) & 1));
+            const long long tile = s_meta[s];
+            // A buffer, row state and info of slot b are free once the epilogue of tile i - 2 is
+            // done (it waited for every chunk's MMAs of that tile)
+            if (i >= 2) tc::mbar_wait(tc::smem_u32(&s_efree[b]), (uint32_t)(((i - 2) >> 1) & 1));
+            if (tile < 0) {
+                if (t == 0) s_info[b].tile = -1;
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[b]));
+                break;
+            }
+            const uint8_t *stage = smem + L.ring + s * L.stage_bytes;
+            const float *sx = reinterpret_cast<const float *>(stage);
+            const int32_t *sa = reinterpret_cast<const int32_t *>(stage + kCRows * DP * 4);
+            const float *su = reinterpret_cast<const float *>(stage + kCRows * DP * 4 + kCRows * 4);
+            const int vrows = (int)(n - tile * kCRows < kCRows ? n - tile * kCRows : kCRows);
+            const int A = sa[vrows >> 1];
+            int ms;
+            if (mA[mcur] == A) ms = mcur;
+            else if (mA[mcur ^ 1] == A) ms = mcur ^ 1;
+            else {
+                ms = mcur ^ 1;   // every prep thread finished the tiles that read this slot
+                if (t == 0) {
+                    const uint32_t mb = tc::smem_u32(&s_mbar[ms]);
+                    tc::mbar_arrive_tx(mb, NMETA * 8);
+                    tc::bulk_g2s(sbase + L.meta + (uint32_t)(ms * NMETA * 8), p.Mc + (int64_t)A * NMETA, NMETA * 8, mb);
+                }
+                tc::mbar_wait(tc::smem_u32(&s_mbar[ms]), mpar[ms]);
+                mpar[ms] ^= 1u;
+                mA[ms] = A;
+            }
+            mcur = ms;
+            const float2 *meta = meta0 + ms * NMETA;
+
+            const int64_t row = tile * kCRows + t;
+            const bool valid = row < n;
+            float x[DP];
+#pragma unroll
+            for (int j = 0; j < DP; j += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(sx + t * DP + j);
+                x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+            }
+            const int aold = valid ? sa[t] : 0;
+            const float uu = valid ? __fadd_ru(su[t], sF[aold]) : 0.f;       // u += f(a)
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_sfree[s]));     // the stage is read
+            const bool c1 = valid && uu <= sS[aold];                           // clause 1
+            const bool active = valid && !c1;
+            const bool misfit = active && aold != A;
+            c_clause1 += c1;
+            TccRow st;
+            st.a = aold; st.uu = uu; st.xx = 0.f; st.ut = 0.f; st.p = 0; st.pad = 0;
+            st.own = misfit ? p.rank[(int64_t)A * k + aold] : -1;
+            st.flags = (valid ? 1 : 0) | (active ? 2 : 0) | (misfit ? 4 : 0);
+            if (active) {
+                float xh[DP];
+                float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < DP; j += 4) {
+                    const float4 c = Cn.ld(A, DP, j);
+                    const float2 t0 = add2(make_float2(x[j], x[j + 1]), make_float2(c.x, c.y));
+                    const float2 t1 = add2(make_float2(x[j + 2], x[j + 3]), make_float2(c.z, c.w));
+                    xh[j] = t0.x; xh[j + 1] = t0.y; xh[j + 2] = t1.x; xh[j + 3] = t1.y;
+                    acc0 = fma2(t0, t0, acc0);
+                    acc1 = fma2(t1, t1, acc1);
+                }
+                const float2 s2 = add2(acc0, acc1);
+                const float xx = s2.x + s2.y;
+                st.xx = xx;
+                float T;
+                if (!misfit) {
+                    st.ut = upper_d(xx, p.g_up, eps);
+                    T = st.ut;
+                } else {
+                    // own distance in the direct form; columns by the triangle bound around A
+                    const float qo = dist2<DP, CSMEM>(x, Cn, aold);
+                    st.ut = upper_d(qo, p.g_up, eps);
+                    T = __fmul_ru(__fadd_ru(st.ut, upper_d(xx, p.g_up, eps)), 0.5f);
+                }
+                st.p = min(count_below2<NMETA>(meta, T), ncols);
+                const uint32_t abuf = sbase + L.aop + (uint32_t)(b * kCRows * KA * 4);
+#pragma unroll
+                for (int j = 0; j < DP; j += 4) {
+                    float h[4], l[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        h[q] = __uint_as_float(__float_as_uint(xh[j + q]) & 0xFFFFE000u);
+                        l[q] = xh[j + q] - h[q];
+                    }
+                    tc::sts128(abuf + tc::op_off(t, j, kCRows), h[0], h[1], h[2], h[3]);
+                    tc::sts128(abuf + tc::op_off(t, DP + j, kCRows), l[0], l[1], l[2], l[3]);
+                }
+                const float xxh = __uint_as_float(__float_as_uint(xx) & 0xFFFFE000u);
+                tc::sts128(abuf + tc::op_off(t, 2 * DP, kCRows), xxh, xx - xxh, 1.f, 1.f);
+            }
+            rstate[b * kCRows + t] = st;
+            const int pw = (__reduce_max_sync(kFull, active ? st.p : 0) + 15) & ~15;
+            if (lane == 0) {
+                s_info[b].pw[warp] = pw;
+                s_info[b].cm[warp] = pw > 0 ? meta[pw - 1].y : 0.f;
+            }
+            tc::fence_async_smem();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (t == 0) {
+                TccInfo &inf = s_info[b];
+                inf.tile = tile;
+                inf.A = A;
+                inf.N = max(max(inf.pw[0], inf.pw[1]), max(inf.pw[2], inf.pw[3]));
+                inf.nch = (inf.N + kCNC - 1) / kCNC;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            tc::fence_before();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[b]));
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) c_clause1 += __shfl_xor_sync(kFull, c_clause1, o);
+        if (lane == 0 && c_clause1) atomicAdd(p.counters + 2, c_clause1);
+    } else if (warp < kCEpiW0 + 4) {
+        // ================= epilogue: running minimum per chunk, decision, queue =============
+        const int ew = warp - kCEpiW0;                 // TMEM lane quadrant
+        const int r = ew * 32 + lane;
+        const uint32_t tlane = s_tmem + ((uint32_t)(ew * 32) << 16);
+        const float eps = *p.eps;
+        constexpr int KT3 = ((3 * DP + 4) + 7) & ~7;       // the products of k_mti_tc's TF32x3 form
+        const float kappa = 2.f * (58.f + DP / 4.f + KT3 / 2.f) * 5.9604645e-8f;   // k_mti_tc's κ
+        unsigned long long c_dists = 0, c_cols = 0, c_queued = 0;
+        uint32_t g = 0;
+        for (int i = 0;; ++i) {
+            const int b = i & 1;
+            tc::mbar_wait(tc::smem_u32(&s_aready[b]), (uint32_t)((i >> 1) & 1));
+            tc::fence_after();
+            const TccInfo inf = s_info[b];
+            if (inf.tile < 0) break;
+            const TccRow st = rstate[b * kCRows + r];
+            const bool valid = st.flags & 1, active = st.flags & 2, misfit = st.flags & 4;
+            const int pw = inf.pw[ew];
+            float m = INFINITY;
+            for (int ch = 0; ch < inf.nch; ++ch, ++g) {
+                const int j = g & 1;
+                tc::mbar_wait(tc::smem_u32(&s_tfull[j]), (g >> 1) & 1);
+                tc::fence_after();
+                const int c0 = ch * kCNC;
+                const int cend = min(kCNC, pw - c0);
+                for (int cc = 0; cc < cend; cc += 16) {
+                    uint32_t rr[16];
+                    tc::tmem_ld16(tlane + (uint32_t)(j * kCNC + cc), rr);
+                    const int base = c0 + cc;
+                    if (__any_sync(kFull, st.own >= base && st.own < base + 16)) {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q)
+                            if (base + q == st.own) rr[q] = 0x7f800000u;   // the own cluster is no rival
+                    }
+#pragma unroll
+                    for (int q = 0; q < 16; q += 2) m = tcc_fmin3(m, __uint_as_float(rr[q]), __uint_as_float(rr[q + 1]));
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_tfree[j]));
+            }
+            if (lane == 0) c_cols += (unsigned long long)pw;
+            bool decided = false;
+            if (active) {
+                const float cmax = inf.cm[ew];
+                const float E = __fmul_ru(kappa, __fadd_ru(st.xx, cmax));
+                const float epsr = __fadd_ru(eps, __fmul_ru(1.2e-7f, __fadd_ru(sqrt_up(st.xx), sqrt_up(cmax))));
+                const float ue = __fadd_ru(st.ut, epsr);
+                const float thr = __fadd_ru(__fmul_ru(ue, ue), E);
+                decided = m > thr && (!misfit || lower_d(st.xx, p.g_dn, eps) > st.ut);
+                if (decided)
+                    c_dists += 1ull + (unsigned long long)(misfit ? count_below_nl(p.NL + (int64_t)st.a * p.ks, k - 1, st.ut)
+                                                                  : st.p);
+            }
+            const bool qd = active && !decided;
+            const unsigned qm = __ballot_sync(kFull, qd);
+            const int64_t tile = inf.tile;
+            const int64_t grp = tile * 4 + ew;
+            if (tile * kCRows + ew * 32 < n) {
+                if (qd) p.qrow[grp * 32 + __popc(qm & ((1u << lane) - 1u))] = (int)(tile * kCRows + r);
+                if (lane == 0) p.qcnt[grp] = __popc(qm);
+            }
+            c_queued += qd;
+            if (valid) p.u[tile * kCRows + r] = decided ? st.ut : st.uu;
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_efree[b]));
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            c_dists += __shfl_xor_sync(kFull, c_dists, o);
+            c_queued += __shfl_xor_sync(kFull, c_queued, o);
+        }
+        if (lane == 0) {
+            if (c_dists) atomicAdd(p.counters + 1, c_dists);
+            if (c_cols) atomicAdd(p.counters + 4, c_cols);
+            if (c_queued) atomicAdd(p.counters + 5, c_queued);
+        }
+    }
+    __syncwarp();
+    tc::fence_before();
+    __syncthreads();
+    if (warp == kCMmaW)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(s_tmem), "r"(2 * kCNC));
+}
+
+// S1 (tensor-chunked part): per cluster c, the B operand chunks and column metadata of its
+// neighbour list (ascending H, as NL[c]); run after k_prep.
+//   column j (centroid c_j = NL[c][j]): c' = fp32(C[c_j]) - fp32(C[c]) (RN), split TF32 hi/lo (RN):
+//     [-2 c'hi | -2 c'lo | 1, 1, cc_hi, cc_lo, 0, 0, 0, 0],  cc = |c'|^2;  chunk j / 128, row j % 128
+//   meta j: {H (fp32, rounded down; NaN past the list), prefix max of |c'|^2 rounded up}
+//   columns past the k-1 neighbours: q = xx + 1e30 (never a winner)
+__global__ void k_prep_tcc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nch, int nmeta,
+                           float *Bc, float2 *Mc, int16_t *rank)
+{
+    // rank[c][c'] = position of c' in c's neighbour list (the epilogue's own column)
+    for (int j = threadIdx.x; j < k - 1; j += blockDim.x)
+        rank[(int64_t)blockIdx.x * k + key_c(NL[(int64_t)blockIdx.x * ks + j])] = (int16_t)j;
+    extern __shared__ float scc[];
+    const int c = blockIdx.x, KA = tcc_ka(DP);
+    const double *Cc = C + (int64_t)c * d;
+    const uint64_t *nl = NL + (int64_t)c * ks;
+    const int ncol = nch * kCNC;
+    for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
+        const bool real = j < k - 1;
+        const int cj = real ? key_c(nl[j]) : c;
+        const double *Cj = C + (int64_t)cj * d;
+        float *B = Bc + ((int64_t)c * nch + j / kCNC) * kCNC * KA;
+        const int jr = j % kCNC;
+        double cn2 = 0.0;
+        for (int e = 0; e < DP; ++e) {
+            const float v = (real && e < d) ? __fsub_rn((float)Cj[e], (float)Cc[e]) : 0.f;
+            const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(__fsub_rn(v, hi));
+            cn2 += (double)v * (double)v;
+            B[tc::op_off(jr, e, kCNC) / 4] = -2.f * hi;
+            B[tc::op_off(jr, DP + e, kCNC) / 4] = -2.f * lo;
+        }
+        const float ccf = real ? (float)cn2 : 1e30f;
+        const float cch = tc::tf32_rna(ccf);
+        const float ccl = real ? tc::tf32_rna((float)(cn2 - (double)cch)) : 0.f;
+        B[tc::op_off(jr, 2 * DP, kCNC) / 4] = 1.f;
+        B[tc::op_off(jr, 2 * DP + 1, kCNC) / 4] = 1.f;
+        B[tc::op_off(jr, 2 * DP + 2, kCNC) / 4] = cch;
+        B[tc::op_off(jr, 2 * DP + 3, kCNC) / 4] = ccl;
+        for (int e = 2 * DP + 4; e < KA; ++e) B[tc::op_off(jr, e, kCNC) / 4] = 0.f;
+        if (j < nmeta) scc[j] = real ? __double2float_ru(cn2 * (1.0 + 1e-12)) : 0.f;
+    }
+    for (int j = threadIdx.x; j < nmeta; j += blockDim.x) {
+        if (j >= ncol) scc[j] = 0.f;
+        Mc[(int64_t)c * nmeta + j].x = j < k - 1 ? key_h(nl[j]) : __int_as_float(0x7fc00000);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int j = 0; j < nmeta; ++j) { m = fmaxf(m, scc[j]); Mc[(int64_t)c * nmeta + j].y = m; }
+    }
+}
+
+cudaError_t launch_prep_tcc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nch, int nmeta,
+                            float *Bc, float2 *Mc, int16_t *rank, cudaStream_t st)
+{
+    k_prep_tcc<<<k, 128, (size_t)nmeta * sizeof(float), st>>>(C, NL, k, d, DP, ks, nch, nmeta, Bc, Mc, rank);
+    return cudaGetLastError();
+}
+
+int tcc_nch_host(int k) { return std::max(1, (k - 1 + kCNC - 1) / kCNC); }
+int tcc_ka_host(int DP) { return tcc_ka(DP); }
+int tcc_nmeta_host(int k) { int m = 16; while (m < k) m <<= 1; return m; }
+
+static int tcc_optin()
+{
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return optin;
+}
+
+// shared memory the chunked tensor-core screen needs (0 if it does not fit one SM)
+size_t tcc_smem(int DP, bool csmem, int k)
+{
+    const TccCfg L = tcc_cfg(DP, csmem, k, tcc_nmeta_host(k));
+    return L.total + 2048 <= tcc_optin() ? (size_t)L.total : 0;
+}
+
+template <int DP, bool CSMEM, int NMETA>
+static cudaError_t launch_tcc_t(const AssignParams &p, const TccCfg &L, int grid, cudaStream_t st)
+{
+    cudaError_t e = cudaFuncSetAttribute(k_tcc<DP, CSMEM, NMETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+    if (e != cudaSuccess) return e;
+    k_tcc<DP, CSMEM, NMETA><<<grid, kCThreads, L.total, st>>>(p, L);
+    return cudaGetLastError();
+}
+
+template <int DP, bool CSMEM>
+static cudaError_t launch_tcc_m(const AssignParams &p, const TccCfg &L, int nmeta, int grid, cudaStream_t st)
+{
+    switch (nmeta) {
+    case 16: return launch_tcc_t<DP, CSMEM, 16>(p, L, grid, st);
+    case 32: return launch_tcc_t<DP, CSMEM, 32>(p, L, grid, st);
+    case 64: return launch_tcc_t<DP, CSMEM, 64>(p, L, grid, st);
+    case 128: return launch_tcc_t<DP, CSMEM, 128>(p, L, grid, st);
+    case 256: return launch_tcc_t<DP, CSMEM, 256>(p, L, grid, st);
+    case 512: return launch_tcc_t<DP, CSMEM, 512>(p, L, grid, st);
+    case 1024: return launch_tcc_t<DP, CSMEM, 1024>(p, L, grid, st);
+    case 2048: return launch_tcc_t<DP, CSMEM, 2048>(p, L, grid, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tcc(int DP, bool csmem, const AssignParams &p, int num_sms, cudaStream_t st)
+{
+    const int nmeta = tcc_nmeta_host(p.k);
+    const TccCfg L = tcc_cfg(DP, csmem, p.k, nmeta);
+    switch (DP * 2 + (csmem ? 1 : 0)) {
+    case 16: return launch_tcc_m<8, false>(p, L, nmeta, num_sms, st);
+    case 17: return launch_tcc_m<8, true>(p, L, nmeta, num_sms, st);
+    case 32: return launch_tcc_m<16, false>(p, L, nmeta, num_sms, st);
+    case 33: return launch_tcc_m<16, true>(p, L, nmeta, num_sms, st);
+    case 64: return launch_tcc_m<32, false>(p, L, nmeta, num_sms, st);
+    case 65: return launch_tcc_m<32, true>(p, L, nmeta, num_sms, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace km

@@ -80,7 +80,7 @@ class KMeans:
         o.resort_fraction = resort_fraction
         o.engine = {"auto": C.KM_ENGINE_AUTO, "cuda": C.KM_ENGINE_CUDA_CORE,
                     "tensor": C.KM_ENGINE_TENSOR, "screen": C.KM_ENGINE_SCREEN,
-                    "tensor_screen": C.KM_ENGINE_TENSOR_SCREEN}[engine]
+                    "tensor_screen": C.KM_ENGINE_TENSOR_SCREEN, "tensor_chunked": C.KM_ENGINE_TENSOR_CHUNKED}[engine]
         o.spherical = int(bool(spherical))
         o.no_graph = int(not graph)
         o.force_comm = int(bool(force_comm))

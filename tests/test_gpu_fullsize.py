@@ -49,7 +49,7 @@ def _independent_checks(X, a, u, Cused, rng, m):
     assert not bad.any(), int(bad.sum())
 
 
-@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen", "tensor_chunked"])
 @pytest.mark.parametrize("name", ["c3", "c4", "c5"])
 def test_full_size_trajectory(name, engine):
     path = os.path.join(GOLD, f"traj_{name}.json")
@@ -64,7 +64,7 @@ def test_full_size_trajectory(name, engine):
     assert sha256_points(X) == g["sha256_X"], "synthetic input differs from the golden run's"
     C0 = X[idx].astype(np.float64)
     km = KMeans(torch.from_numpy(X).cuda(), C0, prune="mti", engine=engine)
-    assert km.engine == {"cuda": "k_walk", "screen": "k_screen", "tensor_screen": "k_mti_tc_screen"}[engine]
+    assert km.engine == {"cuda": "k_walk", "screen": "k_screen", "tensor_screen": "k_mti_tc_screen", "tensor_chunked": "k_tcc"}[engine]
     rng = np.random.default_rng(101)
     T = g["iterations"]
     check_at = {2, T}

@@ -92,7 +92,7 @@ def test_B3_half_factor_on_gpu():
 
 
 # ---- seeded configs, free-running (strict tier) -------------------------------------------
-@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("mti", "screen"), ("mti", "tensor_screen"), ("none", "auto")])
+@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("mti", "screen"), ("mti", "tensor_screen"), ("mti", "tensor_chunked"), ("none", "auto")])
 def test_c1_free_running(prune, engine):
     X, idx, _ = make_config("c1")
     C0 = X[idx].astype(float)
@@ -107,7 +107,7 @@ def test_c1_free_running(prune, engine):
         assert np.all(np.abs(gc - r.clause1) <= 1e-3 * 10000 + 1)
 
 
-@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("mti", "screen"), ("mti", "tensor_screen"), ("none", "auto")])
+@pytest.mark.parametrize("prune,engine", [("mti", "tensor"), ("mti", "cuda"), ("mti", "screen"), ("mti", "tensor_screen"), ("mti", "tensor_chunked"), ("none", "auto")])
 def test_c2_free_running(prune, engine):
     X, idx, _ = make_config("c2")
     C0 = X[idx].astype(float)
@@ -119,7 +119,7 @@ def test_c2_free_running(prune, engine):
         assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
-@pytest.mark.parametrize("engine", ["tensor", "cuda", "screen", "tensor_screen"])
+@pytest.mark.parametrize("engine", ["tensor", "cuda", "screen", "tensor_screen", "tensor_chunked"])
 @pytest.mark.parametrize("name,n,iters", [("c3", 2_000_000, 30), ("c4", 1_000_000, 30)])
 def test_spectral_shaped_free_running(name, n, iters, engine):
     X, idx, _ = make_config(name, n=n)
@@ -131,7 +131,7 @@ def test_spectral_shaped_free_running(name, n, iters, engine):
     assert np.all(np.abs(gd - r.dists) <= 1e-3 * r.dists)
 
 
-@pytest.mark.parametrize("engine", ["tensor", "cuda", "screen", "tensor_screen"])
+@pytest.mark.parametrize("engine", ["tensor", "cuda", "screen", "tensor_screen", "tensor_chunked"])
 def test_c5_shaped_large_k(engine):
     X, idx, _ = make_config("c5", n=300_000)
     C0 = X[idx].astype(float)
@@ -176,11 +176,11 @@ def test_dims_padding(d, engine):
         assert_strict(gpu_run(X, C0, 60, prune, engine=engine), r)
 
 
-@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen", "tensor_chunked"])
 @pytest.mark.parametrize("n", [1, 5, 31, 33, 257, 1000])
 def test_small_and_ragged_n(n, engine):
     rng = np.random.default_rng(n)
-    X = rng.normal(size=(n, 8 if engine == "tensor_screen" else 4)).astype(np.float32)   # tcgen05: d padded to 8/16/32
+    X = rng.normal(size=(n, 8 if engine.startswith("tensor") else 4)).astype(np.float32)   # tcgen05: d padded to 8/16/32
     k = min(n, 3)
     C0 = X[:k].astype(float)
     r = oracle.lloyd(X, C0, 30, 0, "brute")
@@ -201,7 +201,7 @@ def test_k1_and_k_equals_n():
     assert g["sse"] == 0.0
 
 
-@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen", "tensor_chunked"])
 @pytest.mark.parametrize("policy", ["never", "always", "auto"])
 def test_resort_policies_agree(policy, engine):
     X, idx, _ = make_config("c3", n=400_000)
@@ -241,7 +241,7 @@ def test_usage_errors():
         KMeans(np.ones((10, 2), np.float32), np.array([[0, np.inf], [1, 1]]), check_finite=True)
 
 
-@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen"])
+@pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen", "tensor_chunked"])
 def test_bound_soundness_sampled(engine):
     """u_i >= ||x_i - C_used[a_i]|| (fp64, against the fp64 centroids the pass used) for every row
     after every pass, read through kmeans_get_bounds (u loosened by drift,
