@@ -207,8 +207,9 @@ struct km_ctx {
     // column-chunked tensor-core screen (km_tcc.cu)
     bool use_tcc = false;
     float *Bc = nullptr;
-    float2 *Mc = nullptr;
+    float *Mh = nullptr, *Mx = nullptr;
     int tcc_nch = 0, tcc_nmeta = 0;
+    alignas(64) unsigned char tmap[2][128];   // TMA tensor maps of the two row buffers
     int screen_grid = 0, resolve_grid = 0;
     int64_t launches = 0;
 };
@@ -242,8 +243,8 @@ km_status prep(km_ctx *c)
         c->launches += 1;
     }
     if (c->use_tcc) {
-        KM_CUDA(km::launch_prep_tcc(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->tcc_nch, c->tcc_nmeta, c->Bc, c->Mc,
-                                    c->nlrank, c->st));
+        KM_CUDA(km::launch_prep_tcc(c->C, c->NL, c->k, c->d, c->DP, c->ks, c->tcc_nch, c->tcc_nmeta, c->Bc, c->Mh,
+                                    c->Mx, c->nlrank, c->st));
         c->launches += 1;
     }
     if (c->use_tc) {
@@ -297,7 +298,8 @@ km::AssignParams assign_params(km_ctx *c, int work_slot)
     p.qcnt = c->qcnt;
     p.rank = c->nlrank;
     p.Bc = c->Bc;
-    p.Mc = c->Mc;
+    p.Mh = c->Mh;
+    p.Mx = c->Mx;
     p.tcc_nch = c->tcc_nch;
     return p;
 }
@@ -308,7 +310,7 @@ km_status launch_assign(km_ctx *c, int mode, int work_slot)
     if (c->use_ti && (mode == km::MODE_MTI_REDUCE || mode == km::MODE_DENSE)) {
         KM_CUDA(km::launch_ti(c->DP, c->csmem, mode == km::MODE_DENSE, p, c->L, c->Hm, c->ti_grid, c->st));
     } else if (mode == km::MODE_MTI_REDUCE && c->use_tcc) {
-        KM_CUDA(km::launch_tcc(c->DP, c->csmem, p, c->num_sms, c->st));
+        KM_CUDA(km::launch_tcc(c->DP, c->csmem, p, c->num_sms, c->tmap[c->cur], c->st));
         KM_CUDA(km::launch_resolve(c->DP, c->csmem, p, c->resolve_grid, c->st));
         c->launches += 1;
     } else if (mode == km::MODE_MTI_REDUCE && (c->use_tc || c->use_walk)) {
@@ -569,7 +571,7 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base); cudaFree(c->lohist); cudaFree(c->qmap);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P); cudaFree(c->qrow); cudaFree(c->qcnt); cudaFree(c->nlrank); cudaFree(c->Bc); cudaFree(c->Mc);
+    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P); cudaFree(c->qrow); cudaFree(c->qcnt); cudaFree(c->nlrank); cudaFree(c->Bc); cudaFree(c->Mh); cudaFree(c->Mx);
     cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part); cudaFree(c->L); cudaFree(c->Hm);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -728,12 +730,17 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         c->tcc_nch = km::tcc_nch_host(k);
         c->tcc_nmeta = km::tcc_nmeta_host(k);
         KM_TRY(dalloc(&c->Bc, (size_t)k * c->tcc_nch * 128 * km::tcc_ka_host(DP)));
-        KM_TRY(dalloc(&c->Mc, (size_t)k * c->tcc_nmeta));
+        KM_TRY(dalloc(&c->Mh, (size_t)k * km::tcc_hrow_host(k)));
+        KM_TRY(dalloc(&c->Mx, (size_t)k * c->tcc_nmeta));
         KM_TRY(dalloc(&c->nlrank, (size_t)k * k));
         KM_TRY(dalloc(&c->qrow, (size_t)c->n_alloc));
         KM_TRY(dalloc(&c->qcnt, (size_t)(c->n_alloc / 32)));
         c->resolve_grid = km::resolve_grid(DP, c->csmem, k, c->num_sms);
         c->part_grid = std::max(c->part_grid, std::max(c->resolve_grid, c->num_sms));
+        for (int b = 0; b < 2; ++b) {
+            const int r = km::tcc_make_tmap(c->tmap[b], c->X[b], c->n_alloc, DP);
+            if (r != 0) return fail(KM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
+        }
     }
     const bool want_tc = o->engine == KM_ENGINE_TENSOR || o->engine == KM_ENGINE_TENSOR_SCREEN;
     c->use_tc = km::tc_supported(DP) && c->prune == KM_PRUNE_MTI && k >= 2 && !c->use_ti && want_tc;

@@ -77,7 +77,8 @@ struct AssignParams {
     const int16_t *rank;   // k x k: position of c' in c's neighbour list (tensor-screen epilogue)
     // column-chunked tensor-core screen (k_tcc, km_tcc.cu)
     const float *Bc;       // k x tcc_nch x (128 x (2 DP + 8)): B operand chunks (UMMA K-major)
-    const float2 *Mc;      // k x nmeta: {H, prefix max of |c'|^2 (up)}
+    const float *Mh;       // k x hrow: H of the list, skewed (entry j at j + j / 32), NaN padded
+    const float *Mx;       // k x nmeta: prefix max of |c'|^2 (up)
     int32_t tcc_nch;       // chunks per cluster list
 };
 
@@ -123,9 +124,11 @@ cudaError_t launch_mti_tc(int DP, bool csmem, const AssignParams &p, int grid, b
 cudaError_t launch_prep_tc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nmax,
                            float *Bop, float4 *Bmeta, int16_t *rank, cudaStream_t st);
 cudaError_t launch_resolve(int DP, bool csmem, const AssignParams &p, int g_resolve, cudaStream_t st);
-cudaError_t launch_tcc(int DP, bool csmem, const AssignParams &p, int num_sms, cudaStream_t st);
+cudaError_t launch_tcc(int DP, bool csmem, const AssignParams &p, int num_sms, const void *tmap, cudaStream_t st);
+int tcc_make_tmap(void *out, const float *X, int64_t n_alloc, int DP);
 cudaError_t launch_prep_tcc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nch, int nmeta,
-                            float *Bc, float2 *Mc, int16_t *rank, cudaStream_t st);
+                            float *Bc, float *Mh, float *Mx, int16_t *rank, cudaStream_t st);
+int tcc_hrow_host(int k);
 size_t tcc_smem(int DP, bool csmem, int k);
 int tcc_nch_host(int k);
 int tcc_ka_host(int DP);

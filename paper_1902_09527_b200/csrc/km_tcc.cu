@@ -33,6 +33,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda.h>
+
 #include "km_device.cuh"
 #include "km_kernels.cuh"
 #include "km_tc_common.cuh"
@@ -50,6 +52,9 @@ constexpr int kCStages = 2;
 
 __host__ __device__ constexpr int tcc_ka(int DP) { return 2 * DP + 8; }
 
+// per-row state handed from the prep warps to the epilogue warps, structure of arrays (one
+// 4-byte word per lane: conflict-free), two tile slots
+constexpr int kRowFields = 7;   // a, flags, uu, ut, xx, p, own
 struct TccRow {
     int a;          // assignment before the pass
     int flags;      // bit0 valid, bit1 active (clause 1 failed), bit2 misfit (a != A)
@@ -58,8 +63,21 @@ struct TccRow {
     float xx;       // |x - C^[A]|^2
     int p;          // columns below the row's threshold
     int own;        // misfit: position of a in A's list, else -1
-    int pad;
 };
+__device__ __forceinline__ void row_store(int *base, int b, int r, const TccRow &s)
+{
+    int *q = base + b * kRowFields * kCRows + r;
+    q[0] = s.a; q[kCRows] = s.flags; q[2 * kCRows] = __float_as_int(s.uu); q[3 * kCRows] = __float_as_int(s.ut);
+    q[4 * kCRows] = __float_as_int(s.xx); q[5 * kCRows] = s.p; q[6 * kCRows] = s.own;
+}
+__device__ __forceinline__ TccRow row_load(const int *base, int b, int r)
+{
+    const int *q = base + b * kRowFields * kCRows + r;
+    TccRow s;
+    s.a = q[0]; s.flags = q[kCRows]; s.uu = __int_as_float(q[2 * kCRows]); s.ut = __int_as_float(q[3 * kCRows]);
+    s.xx = __int_as_float(q[4 * kCRows]); s.p = q[5 * kCRows]; s.own = q[6 * kCRows];
+    return s;
+}
 
 struct TccInfo {
     long long tile;  // -1 = end of stream
@@ -72,32 +90,46 @@ struct TccCfg {
     int stage_bytes, ring, aop, bop, meta, rstate, sc, sf, ss, total;
 };
 
+// The row tile [128 x DP] is loaded by a 2-D TMA tensor copy with the hardware swizzle whose span
+// is the row (32 / 64 / 128 B for DP = 8 / 16 / 32): 16-byte piece q of row r lands at piece
+// q ^ f(r), so the lanes of a warp (one row each) read their pieces without bank conflicts
+// (unswizzled 128-byte rows put every lane's piece q in the same banks: 8-way conflicts,
+// measured on C5).  Byte offset o of the dense tile is stored at o ^ (((o >> 7) & M) << 4).
+__host__ __device__ constexpr int tcc_xs(int DP) { return DP * 4; }
+__host__ __device__ constexpr int tcc_swz_mask(int DP) { return DP >= 32 ? 7 : (DP >= 16 ? 3 : 1); }
+__device__ __forceinline__ uint32_t tcc_swz(uint32_t o, int M) { return o ^ (((o >> 7) & (uint32_t)M) << 4); }
+// H of a cluster's list in shared memory, skewed (entry i at i + i / 32) so that the lanes'
+// binary-search probes fall in distinct banks
+__host__ __device__ constexpr int tcc_hs(int nmeta) { return nmeta + nmeta / 32 + 4; }
+
 __host__ __device__ inline TccCfg tcc_cfg(int DP, bool csmem, int k, int nmeta)
 {
     TccCfg L;
     const int KA = tcc_ka(DP);
-    L.stage_bytes = kCRows * DP * 4 + 2 * kCRows * 4;
+    L.stage_bytes = (kCRows * tcc_xs(DP) + 2 * kCRows * 4 + 1023) & ~1023;   // swizzled tiles: 1 KB aligned
     L.ring = 0;
     L.aop = (L.ring + kCStages * L.stage_bytes + 127) & ~127;
     L.bop = L.aop + 2 * kCRows * KA * 4;
     L.meta = L.bop + 2 * kCNC * KA * 4;
-    L.rstate = L.meta + 2 * nmeta * 8;
-    L.sc = L.rstate + 2 * kCRows * (int)sizeof(TccRow);
+    L.rstate = L.meta + ((2 * tcc_hs(nmeta) * 4 + 15) & ~15);
+    L.sc = L.rstate + 2 * kCRows * kRowFields * 4;
     L.sf = L.sc + (csmem ? k * DP * 4 : 0);
     L.ss = L.sf + ((k + 3) & ~3) * 4;
     L.total = L.ss + ((k + 3) & ~3) * 4;
     return L;
 }
 
-// #{j < M : meta[j].x < T} (ascending, NaN padded), M a power of two
+// #{j < M : h[j] < T} over a skewed row (entry j at j + j / 32; ascending, NaN padded)
 template <int M>
-__device__ __forceinline__ int count_below2(const float2 *meta, float T)
+__device__ __forceinline__ int count_below_k(const float *h, float T)
 {
     int base = 0;
 #pragma unroll
-    for (int half = M >> 1; half >= 1; half >>= 1)
-        base = meta[base + half - 1].x < T ? base + half : base;
-    return base + (meta[base].x < T ? 1 : 0);
+    for (int half = M >> 1; half >= 1; half >>= 1) {
+        const int j = base + half - 1;
+        base = h[j + (j >> 5)] < T ? base + half : base;
+    }
+    return base + (h[base + (base >> 5)] < T ? 1 : 0);
 }
 
 __device__ __forceinline__ float tcc_fmin3(float a, float b, float c)
@@ -109,7 +141,7 @@ __device__ __forceinline__ float tcc_fmin3(float a, float b, float c)
 
 template <int DP, bool CSMEM, int NMETA>
 __global__ void __launch_bounds__(kCThreads, 1)
-k_tcc(AssignParams p, TccCfg L)
+k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
 {
     constexpr int KA = tcc_ka(DP);
     constexpr uint32_t kBBytes = kCNC * KA * 4;
@@ -126,8 +158,10 @@ k_tcc(AssignParams p, TccCfg L)
     float *sC = reinterpret_cast<float *>(smem + L.sc);
     float *sF = reinterpret_cast<float *>(smem + L.sf);
     float *sS = reinterpret_cast<float *>(smem + L.ss);
-    TccRow *rstate = reinterpret_cast<TccRow *>(smem + L.rstate);
-    const float2 *meta0 = reinterpret_cast<const float2 *>(smem + L.meta);
+    int *rstate = reinterpret_cast<int *>(smem + L.rstate);
+    const float *meta0 = reinterpret_cast<const float *>(smem + L.meta);
+    constexpr int XS = tcc_xs(DP);
+    constexpr int HS = tcc_hs(NMETA);
 
     if (CSMEM) {
         const float4 *src = reinterpret_cast<const float4 *>(p.Cneg);
@@ -167,7 +201,7 @@ k_tcc(AssignParams p, TccCfg L)
     const int64_t ntiles = (n + kCRows - 1) / kCRows;
 
     if (warp == kCProdW) {
-        // ================= producer: row tiles [x | a | u] -> ring stages ==================
+        // ================= producer: row tiles [x (swizzled) | a | u] -> ring stages ========
         if (lane == 0) {
             const int G = p.tile_chunk;
             int64_t q_next = 0, q_end = 0;
@@ -187,7 +221,9 @@ k_tcc(AssignParams p, TccCfg L)
                 const uint32_t xb = kCRows * DP * 4, ab = kCRows * 4;
                 tc::mbar_arrive_tx(mb, xb + 2 * ab);
                 const uint32_t dst = sbase + L.ring + s * L.stage_bytes;
-                tc::bulk_g2s(dst, p.X + tl * kCRows * DP, xb, mb);
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                             :: "r"(dst), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"((int)(tl * kCRows)), "r"(mb)
+                             : "memory");
                 tc::bulk_g2s(dst + xb, p.a + tl * kCRows, ab, mb);
                 tc::bulk_g2s(dst + xb + ab, p.u + tl * kCRows, ab, mb);
             }
@@ -266,9 +302,9 @@ k_tcc(AssignParams p, TccCfg L)
                 break;
             }
             const uint8_t *stage = smem + L.ring + s * L.stage_bytes;
-            const float *sx = reinterpret_cast<const float *>(stage);
-            const int32_t *sa = reinterpret_cast<const int32_t *>(stage + kCRows * DP * 4);
-            const float *su = reinterpret_cast<const float *>(stage + kCRows * DP * 4 + kCRows * 4);
+            const uint32_t sxa = tc::smem_u32(stage);                                // swizzled row tile
+            const int32_t *sa = reinterpret_cast<const int32_t *>(stage + kCRows * XS);
+            const float *su = reinterpret_cast<const float *>(stage + kCRows * XS + kCRows * 4);
             const int vrows = (int)(n - tile * kCRows < kCRows ? n - tile * kCRows : kCRows);
             const int A = sa[vrows >> 1];
             int ms;
@@ -278,22 +314,23 @@ k_tcc(AssignParams p, TccCfg L)
                 ms = mcur ^ 1;   // every prep thread finished the tiles that read this slot
                 if (t == 0) {
                     const uint32_t mb = tc::smem_u32(&s_mbar[ms]);
-                    tc::mbar_arrive_tx(mb, NMETA * 8);
-                    tc::bulk_g2s(sbase + L.meta + (uint32_t)(ms * NMETA * 8), p.Mc + (int64_t)A * NMETA, NMETA * 8, mb);
+                    const uint32_t hb = (uint32_t)(((HS * 4) + 15) & ~15);
+                    tc::mbar_arrive_tx(mb, hb);
+                    tc::bulk_g2s(sbase + L.meta + (uint32_t)(ms * hb), p.Mh + (int64_t)A * (hb / 4), hb, mb);
                 }
                 tc::mbar_wait(tc::smem_u32(&s_mbar[ms]), mpar[ms]);
                 mpar[ms] ^= 1u;
                 mA[ms] = A;
             }
             mcur = ms;
-            const float2 *meta = meta0 + ms * NMETA;
+            const float *meta = meta0 + ms * ((((HS * 4) + 15) & ~15) / 4);
 
             const int64_t row = tile * kCRows + t;
             const bool valid = row < n;
             float x[DP];
 #pragma unroll
             for (int j = 0; j < DP; j += 4) {
-                const float4 v = *reinterpret_cast<const float4 *>(sx + t * DP + j);
+                const float4 v = lds128(sxa + tcc_swz((uint32_t)(t * XS + j * 4), tcc_swz_mask(DP)));
                 x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
             }
             const int aold = valid ? sa[t] : 0;
@@ -305,7 +342,7 @@ k_tcc(AssignParams p, TccCfg L)
             const bool misfit = active && aold != A;
             c_clause1 += c1;
             TccRow st;
-            st.a = aold; st.uu = uu; st.xx = 0.f; st.ut = 0.f; st.p = 0; st.pad = 0;
+            st.a = aold; st.uu = uu; st.xx = 0.f; st.ut = 0.f; st.p = 0;
             st.own = misfit ? p.rank[(int64_t)A * k + aold] : -1;
             st.flags = (valid ? 1 : 0) | (active ? 2 : 0) | (misfit ? 4 : 0);
             if (active) {
@@ -333,7 +370,7 @@ k_tcc(AssignParams p, TccCfg L)
                     st.ut = upper_d(qo, p.g_up, eps);
                     T = __fmul_ru(__fadd_ru(st.ut, upper_d(xx, p.g_up, eps)), 0.5f);
                 }
-                st.p = min(count_below2<NMETA>(meta, T), ncols);
+                st.p = min(count_below_k<NMETA>(meta, T), ncols);
                 const uint32_t abuf = sbase + L.aop + (uint32_t)(b * kCRows * KA * 4);
 #pragma unroll
                 for (int j = 0; j < DP; j += 4) {
@@ -349,11 +386,11 @@ k_tcc(AssignParams p, TccCfg L)
                 const float xxh = __uint_as_float(__float_as_uint(xx) & 0xFFFFE000u);
                 tc::sts128(abuf + tc::op_off(t, 2 * DP, kCRows), xxh, xx - xxh, 1.f, 1.f);
             }
-            rstate[b * kCRows + t] = st;
+            row_store(rstate, b, t, st);
             const int pw = (__reduce_max_sync(kFull, active ? st.p : 0) + 15) & ~15;
             if (lane == 0) {
                 s_info[b].pw[warp] = pw;
-                s_info[b].cm[warp] = pw > 0 ? meta[pw - 1].y : 0.f;
+                s_info[b].cm[warp] = pw > 0 ? __ldg(p.Mx + (int64_t)A * NMETA + pw - 1) : 0.f;
             }
             tc::fence_async_smem();
             asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -387,7 +424,7 @@ k_tcc(AssignParams p, TccCfg L)
             tc::fence_after();
             const TccInfo inf = s_info[b];
             if (inf.tile < 0) break;
-            const TccRow st = rstate[b * kCRows + r];
+            const TccRow st = row_load(rstate, b, r);
             const bool valid = st.flags & 1, active = st.flags & 2, misfit = st.flags & 4;
             const int pw = inf.pw[ew];
             float m = INFINITY;
@@ -397,17 +434,23 @@ k_tcc(AssignParams p, TccCfg L)
                 tc::fence_after();
                 const int c0 = ch * kCNC;
                 const int cend = min(kCNC, pw - c0);
-                for (int cc = 0; cc < cend; cc += 16) {
-                    uint32_t rr[16];
-                    tc::tmem_ld16(tlane + (uint32_t)(j * kCNC + cc), rr);
-                    const int base = c0 + cc;
-                    if (__any_sync(kFull, st.own >= base && st.own < base + 16)) {
+                for (int cc = 0; cc < cend; cc += 32) {    // cend: a multiple of 16
+                    uint32_t rr[32];
+                    if (cend - cc >= 32) tc::tmem_ld32(tlane + (uint32_t)(j * kCNC + cc), rr);
+                    else {
+                        uint32_t h16[16];
+                        tc::tmem_ld16(tlane + (uint32_t)(j * kCNC + cc), h16);
 #pragma unroll
-                        for (int q = 0; q < 16; ++q)
+                        for (int q = 0; q < 16; ++q) { rr[q] = h16[q]; rr[16 + q] = 0x7f800000u; }
+                    }
+                    const int base = c0 + cc;
+                    if (__any_sync(kFull, st.own >= base && st.own < base + 32)) {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q)
                             if (base + q == st.own) rr[q] = 0x7f800000u;   // the own cluster is no rival
                     }
 #pragma unroll
-                    for (int q = 0; q < 16; q += 2) m = tcc_fmin3(m, __uint_as_float(rr[q]), __uint_as_float(rr[q + 1]));
+                    for (int q = 0; q < 32; q += 2) m = tcc_fmin3(m, __uint_as_float(rr[q]), __uint_as_float(rr[q + 1]));
                 }
                 tc::fence_before();
                 __syncwarp();
@@ -464,7 +507,7 @@ k_tcc(AssignParams p, TccCfg L)
 //   meta j: {H (fp32, rounded down; NaN past the list), prefix max of |c'|^2 rounded up}
 //   columns past the k-1 neighbours: q = xx + 1e30 (never a winner)
 __global__ void k_prep_tcc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nch, int nmeta,
-                           float *Bc, float2 *Mc, int16_t *rank)
+                           float *Bc, float *Mh, float *Mx, int16_t *rank)
 {
     // rank[c][c'] = position of c' in c's neighbour list (the epilogue's own column)
     for (int j = threadIdx.x; j < k - 1; j += blockDim.x)
@@ -498,27 +541,31 @@ __global__ void k_prep_tcc(const double *C, const uint64_t *NL, int k, int d, in
         for (int e = 2 * DP + 4; e < KA; ++e) B[tc::op_off(jr, e, kCNC) / 4] = 0.f;
         if (j < nmeta) scc[j] = real ? __double2float_ru(cn2 * (1.0 + 1e-12)) : 0.f;
     }
+    const int hrow = ((tcc_hs(nmeta) * 4 + 15) & ~15) / 4;   // skewed H row (padded to 16 B)
+    for (int j = threadIdx.x; j < hrow; j += blockDim.x) Mh[(int64_t)c * hrow + j] = __int_as_float(0x7fc00000);
+    __syncthreads();
     for (int j = threadIdx.x; j < nmeta; j += blockDim.x) {
         if (j >= ncol) scc[j] = 0.f;
-        Mc[(int64_t)c * nmeta + j].x = j < k - 1 ? key_h(nl[j]) : __int_as_float(0x7fc00000);
+        Mh[(int64_t)c * hrow + j + (j >> 5)] = j < k - 1 ? key_h(nl[j]) : __int_as_float(0x7fc00000);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         float m = 0.f;
-        for (int j = 0; j < nmeta; ++j) { m = fmaxf(m, scc[j]); Mc[(int64_t)c * nmeta + j].y = m; }
+        for (int j = 0; j < nmeta; ++j) { m = fmaxf(m, scc[j]); Mx[(int64_t)c * nmeta + j] = m; }
     }
 }
 
 cudaError_t launch_prep_tcc(const double *C, const uint64_t *NL, int k, int d, int DP, int ks, int nch, int nmeta,
-                            float *Bc, float2 *Mc, int16_t *rank, cudaStream_t st)
+                            float *Bc, float *Mh, float *Mx, int16_t *rank, cudaStream_t st)
 {
-    k_prep_tcc<<<k, 128, (size_t)nmeta * sizeof(float), st>>>(C, NL, k, d, DP, ks, nch, nmeta, Bc, Mc, rank);
+    k_prep_tcc<<<k, 128, (size_t)nmeta * sizeof(float), st>>>(C, NL, k, d, DP, ks, nch, nmeta, Bc, Mh, Mx, rank);
     return cudaGetLastError();
 }
 
 int tcc_nch_host(int k) { return std::max(1, (k - 1 + kCNC - 1) / kCNC); }
 int tcc_ka_host(int DP) { return tcc_ka(DP); }
 int tcc_nmeta_host(int k) { int m = 16; while (m < k) m <<= 1; return m; }
+int tcc_hrow_host(int k) { return ((tcc_hs(tcc_nmeta_host(k)) * 4 + 15) & ~15) / 4; }
 
 static int tcc_optin()
 {
@@ -536,43 +583,72 @@ size_t tcc_smem(int DP, bool csmem, int k)
 }
 
 template <int DP, bool CSMEM, int NMETA>
-static cudaError_t launch_tcc_t(const AssignParams &p, const TccCfg &L, int grid, cudaStream_t st)
+static cudaError_t launch_tcc_t(const AssignParams &p, const TccCfg &L, int grid, const CUtensorMap &tm, cudaStream_t st)
 {
     cudaError_t e = cudaFuncSetAttribute(k_tcc<DP, CSMEM, NMETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
     if (e != cudaSuccess) return e;
-    k_tcc<DP, CSMEM, NMETA><<<grid, kCThreads, L.total, st>>>(p, L);
+    k_tcc<DP, CSMEM, NMETA><<<grid, kCThreads, L.total, st>>>(p, L, tm);
     return cudaGetLastError();
 }
 
 template <int DP, bool CSMEM>
-static cudaError_t launch_tcc_m(const AssignParams &p, const TccCfg &L, int nmeta, int grid, cudaStream_t st)
+static cudaError_t launch_tcc_m(const AssignParams &p, const TccCfg &L, int nmeta, int grid, const CUtensorMap &tm,
+                                cudaStream_t st)
 {
     switch (nmeta) {
-    case 16: return launch_tcc_t<DP, CSMEM, 16>(p, L, grid, st);
-    case 32: return launch_tcc_t<DP, CSMEM, 32>(p, L, grid, st);
-    case 64: return launch_tcc_t<DP, CSMEM, 64>(p, L, grid, st);
-    case 128: return launch_tcc_t<DP, CSMEM, 128>(p, L, grid, st);
-    case 256: return launch_tcc_t<DP, CSMEM, 256>(p, L, grid, st);
-    case 512: return launch_tcc_t<DP, CSMEM, 512>(p, L, grid, st);
-    case 1024: return launch_tcc_t<DP, CSMEM, 1024>(p, L, grid, st);
-    case 2048: return launch_tcc_t<DP, CSMEM, 2048>(p, L, grid, st);
+    case 16: return launch_tcc_t<DP, CSMEM, 16>(p, L, grid, tm, st);
+    case 32: return launch_tcc_t<DP, CSMEM, 32>(p, L, grid, tm, st);
+    case 64: return launch_tcc_t<DP, CSMEM, 64>(p, L, grid, tm, st);
+    case 128: return launch_tcc_t<DP, CSMEM, 128>(p, L, grid, tm, st);
+    case 256: return launch_tcc_t<DP, CSMEM, 256>(p, L, grid, tm, st);
+    case 512: return launch_tcc_t<DP, CSMEM, 512>(p, L, grid, tm, st);
+    case 1024: return launch_tcc_t<DP, CSMEM, 1024>(p, L, grid, tm, st);
+    case 2048: return launch_tcc_t<DP, CSMEM, 2048>(p, L, grid, tm, st);
     }
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_tcc(int DP, bool csmem, const AssignParams &p, int num_sms, cudaStream_t st)
+// tmap: the CUtensorMap (128 bytes) of the row buffer p.X, from tcc_make_tmap
+cudaError_t launch_tcc(int DP, bool csmem, const AssignParams &p, int num_sms, const void *tmap, cudaStream_t st)
 {
     const int nmeta = tcc_nmeta_host(p.k);
     const TccCfg L = tcc_cfg(DP, csmem, p.k, nmeta);
+    const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(tmap);
     switch (DP * 2 + (csmem ? 1 : 0)) {
-    case 16: return launch_tcc_m<8, false>(p, L, nmeta, num_sms, st);
-    case 17: return launch_tcc_m<8, true>(p, L, nmeta, num_sms, st);
-    case 32: return launch_tcc_m<16, false>(p, L, nmeta, num_sms, st);
-    case 33: return launch_tcc_m<16, true>(p, L, nmeta, num_sms, st);
-    case 64: return launch_tcc_m<32, false>(p, L, nmeta, num_sms, st);
-    case 65: return launch_tcc_m<32, true>(p, L, nmeta, num_sms, st);
+    case 16: return launch_tcc_m<8, false>(p, L, nmeta, num_sms, tm, st);
+    case 17: return launch_tcc_m<8, true>(p, L, nmeta, num_sms, tm, st);
+    case 32: return launch_tcc_m<16, false>(p, L, nmeta, num_sms, tm, st);
+    case 33: return launch_tcc_m<16, true>(p, L, nmeta, num_sms, tm, st);
+    case 64: return launch_tcc_m<32, false>(p, L, nmeta, num_sms, tm, st);
+    case 65: return launch_tcc_m<32, true>(p, L, nmeta, num_sms, tm, st);
     }
     return cudaErrorInvalidValue;
+}
+
+// 2-D tensor map of an n_alloc x DP fp32 row buffer: box 128 rows x DP, the row-span swizzle
+// (tcc_swz); out: 128 bytes, 64-byte aligned.  Returns 0 on success.
+int tcc_make_tmap(void *out, const float *X, int64_t n_alloc, int DP)
+{
+    typedef CUresult (*encode_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static encode_t fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f) return -1;
+        fn = reinterpret_cast<encode_t>(f);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)DP, (cuuint64_t)n_alloc};
+    const cuuint64_t strides[1] = {(cuuint64_t)DP * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)DP, (cuuint32_t)kCRows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = DP >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                           : (DP >= 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    const CUresult r = fn(reinterpret_cast<CUtensorMap *>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X),
+                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
 }  // namespace km
