@@ -59,7 +59,9 @@ enum { KM_PRUNE_MTI = 0, KM_PRUNE_NONE = 1, KM_PRUNE_TI = 2 };
  * whenever the points reassigned since the last sort exceed resort_fraction * n_local. */
 enum { KM_RESORT_AUTO = 0, KM_RESORT_NEVER = 1, KM_RESORT_ALWAYS = 2 };
 
-/* Candidate-evaluation engine of the MTI pass.  AUTO and CUDA_CORE: the CUDA-core
+/* Candidate-evaluation engine of the MTI pass.  AUTO: TENSOR_CHUNKED when d pads
+ * to 32 and k >= 512 (the dense-survivor regime, C5), else CUDA_CORE (measured on B200, DESIGN.md
+ * "Engine choice").  CUDA_CORE: the CUDA-core
  * walk ("k_walk"; "k_walk_skip1" when the previous pass's clause-1 rate exceeds 15 %).  SCREEN:
  * the same walk split in two kernels ("k_screen": every row, minimum candidate value only, the
  * rows that provably stay are decided; "k_resolve": the queued rest, direct form + exact-mode

@@ -717,10 +717,15 @@ km_status create(int64_t n, int32_t d, int32_t k, const float *points, const dou
         c->grid_assign[m] = km::assign_grid(m, DP, c->csmem, k, c->num_sms);
         c->part_grid = std::max(c->part_grid, c->grid_assign[m]);
     }
-    // AUTO: the CUDA-core walk (measured faster than the tensor-core pipeline on C3 and C4 so
-    // far); KM_ENGINE_TENSOR selects the tcgen05 kernel
-    // (k = 1 or another prune mode: the default engines, as for the walk)
-    if (o->engine == KM_ENGINE_TENSOR_CHUNKED && c->prune == KM_PRUNE_MTI && !c->use_ti && k >= 2) {
+    // AUTO (measured on B200 at full size): the column-chunked
+    // tensor-core screen k_tcc when d pads to 32 and k >= kAutoTccK (C5, k = 1000: 11.1 vs 24.5 ms
+    // per pass: a quarter of its active rows need nearly the whole neighbour list, the dense-
+    // survivor regime the tensor cores serve), the CUDA-core walk otherwise (C3 1.56 vs 5.26 ms,
+    // C4 6.27 vs 7.76 ms); k = 1 or another prune mode: the default engines, as for the walk
+    constexpr int kAutoTccK = 512;
+    const bool auto_tcc = o->engine == KM_ENGINE_AUTO && DP == 32 && k >= kAutoTccK &&
+                          km::tcc_smem(DP, c->csmem, k) != 0;
+    if ((o->engine == KM_ENGINE_TENSOR_CHUNKED || auto_tcc) && c->prune == KM_PRUNE_MTI && !c->use_ti && k >= 2) {
         if (!km::tc_supported(DP))
             return fail(KM_EARG, "tensor_chunked engine needs d padded to 8, 16 or 32 (d=%d)", d);
         if (km::tcc_smem(DP, c->csmem, k) == 0)

@@ -43,12 +43,20 @@ namespace km {
 
 constexpr int kCRows = 128;            // rows per tile (MMA M)
 constexpr int kCNC = 128;              // columns per chunk (MMA N <= 128)
-constexpr int kCThreads = 320;
-constexpr int kCPrepW = 4;             // warps 0-3: prep
+constexpr int kCThreads = 448;
+constexpr int kCPrepW = 4;             // warps 0-3: prep group 0 (even tiles)
+constexpr int kCPrepW1 = 10;           // warps 10-13: prep group 1 (odd tiles)
 constexpr int kCEpiW0 = 4;             // warps 4-7: epilogue (TMEM lane quadrant = warp % 4)
 constexpr int kCProdW = 8;             // warp 8: row-tile producer
 constexpr int kCMmaW = 9;              // warp 9: B-chunk loads + MMA issue
 constexpr int kCStages = 2;
+// Slots.  A operand: 2 (released by the MMA commit of the tile's last chunk, not by the epilogue);
+// row state / tile info: kRS (released by the epilogue); TMEM accumulators: kTB x 128 columns.
+// Prep of tile i waits only for the MMAs of tile i - 2, so the epilogue of a tile overlaps the
+// prep and MMAs of the next ones (with one slot ring for all three the period of two tiles was
+// prep + MMA + epilogue: ~4000 cycles per tile on C5, the tensor pipe 23 % busy).
+constexpr int kRS = 4;
+constexpr int kTB = 4;
 
 __host__ __device__ constexpr int tcc_ka(int DP) { return 2 * DP + 8; }
 
@@ -112,7 +120,7 @@ __host__ __device__ inline TccCfg tcc_cfg(int DP, bool csmem, int k, int nmeta)
     L.bop = L.aop + 2 * kCRows * KA * 4;
     L.meta = L.bop + 2 * kCNC * KA * 4;
     L.rstate = L.meta + ((2 * tcc_hs(nmeta) * 4 + 15) & ~15);
-    L.sc = L.rstate + 2 * kCRows * kRowFields * 4;
+    L.sc = L.rstate + kRS * kCRows * kRowFields * 4;
     L.sf = L.sc + (csmem ? k * DP * 4 : 0);
     L.ss = L.sf + ((k + 3) & ~3) * 4;
     L.total = L.ss + ((k + 3) & ~3) * 4;
@@ -147,9 +155,9 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
     constexpr uint32_t kBBytes = kCNC * KA * 4;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t s_full[kCStages], s_sfree[kCStages];
-    __shared__ __align__(8) uint64_t s_aready[2], s_efree[2], s_bfull[2], s_bempty[2], s_tfull[2], s_tfree[2], s_mbar[2];
+    __shared__ __align__(8) uint64_t s_aready[kRS], s_efree[kRS], s_afree[2], s_bfull[2], s_bempty[2], s_tfull[kTB], s_tfree[kTB], s_mbar[2];
     __shared__ long long s_meta[kCStages];
-    __shared__ TccInfo s_info[2];
+    __shared__ TccInfo s_info[kRS];
     __shared__ uint32_t s_tmem;
 
     const int k = p.k;
@@ -175,7 +183,7 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
     }
     if (warp == kCMmaW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(tc::smem_u32(&s_tmem)), "r"(2 * kCNC));
+                     :: "r"(tc::smem_u32(&s_tmem)), "r"(kTB * kCNC));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (t == 0) {
@@ -184,13 +192,18 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
             tc::mbar_init(tc::smem_u32(&s_sfree[s]), kCPrepW);
         }
         for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(tc::smem_u32(&s_aready[b]), kCPrepW);
-            tc::mbar_init(tc::smem_u32(&s_efree[b]), 4);
+            tc::mbar_init(tc::smem_u32(&s_afree[b]), 1);
             tc::mbar_init(tc::smem_u32(&s_bfull[b]), 1);
             tc::mbar_init(tc::smem_u32(&s_bempty[b]), 1);
+            tc::mbar_init(tc::smem_u32(&s_mbar[b]), 1);
+        }
+        for (int b = 0; b < kRS; ++b) {
+            tc::mbar_init(tc::smem_u32(&s_aready[b]), kCPrepW);
+            tc::mbar_init(tc::smem_u32(&s_efree[b]), 4);
+        }
+        for (int b = 0; b < kTB; ++b) {
             tc::mbar_init(tc::smem_u32(&s_tfull[b]), 1);
             tc::mbar_init(tc::smem_u32(&s_tfree[b]), 4);
-            tc::mbar_init(tc::smem_u32(&s_mbar[b]), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -205,19 +218,24 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
         if (lane == 0) {
             const int G = p.tile_chunk;
             int64_t q_next = 0, q_end = 0;
+            int nterm = 0;
             for (int L_ = 0;; ++L_) {
                 const int s = L_ % kCStages;
                 if (L_ >= kCStages) tc::mbar_wait(tc::smem_u32(&s_sfree[s]), (uint32_t)(((L_ / kCStages) - 1) & 1));
-                if (q_next >= q_end) {
+                if (q_next >= q_end && nterm == 0) {
                     const int64_t c = atomicAdd(p.work, 1);
                     q_next = c * G;
                     q_end = q_next + G;
                 }
-                const int64_t tl = q_next < ntiles ? q_next : -1;
+                const int64_t tl = q_next < ntiles && nterm == 0 ? q_next : -1;
                 ++q_next;
                 s_meta[s] = tl;
                 const uint32_t mb = tc::smem_u32(&s_full[s]);
-                if (tl < 0) { tc::mbar_arrive(mb); break; }
+                if (tl < 0) {   // one end-of-stream tile per prep group (stage s is group s's)
+                    tc::mbar_arrive(mb);
+                    if (++nterm == kCStages) break;
+                    continue;
+                }
                 const uint32_t xb = kCRows * DP * 4, ab = kCRows * 4;
                 tc::mbar_arrive_tx(mb, xb + 2 * ab);
                 const uint32_t dst = sbase + L.ring + s * L.stage_bytes;
@@ -234,35 +252,45 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
             const uint32_t idesc_base = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCRows >> 4) << 24);
             const uint32_t bfull[2] = {tc::smem_u32(&s_bfull[0]), tc::smem_u32(&s_bfull[1])};
             const uint32_t bempty[2] = {tc::smem_u32(&s_bempty[0]), tc::smem_u32(&s_bempty[1])};
-            const uint32_t tfull[2] = {tc::smem_u32(&s_tfull[0]), tc::smem_u32(&s_tfull[1])};
-            const uint32_t tfree[2] = {tc::smem_u32(&s_tfree[0]), tc::smem_u32(&s_tfree[1])};
             uint32_t g = 0;                               // chunks issued so far
+            // B slot j holds chunks with ch % 2 == j; a slot still holding the wanted chunk (same
+            // cluster A, same chunk: consecutive tiles of a bucket) is not reloaded
+            int nfill[2] = {0, 0}, tag[2] = {-1, -1};
             for (int i = 0;; ++i) {
-                const int b = i & 1;
-                tc::mbar_wait(tc::smem_u32(&s_aready[b]), (uint32_t)((i >> 1) & 1));
+                const int b = i & 1, rs = i % kRS;
+                tc::mbar_wait(tc::smem_u32(&s_aready[rs]), (uint32_t)((i / kRS) & 1));
                 tc::fence_after();
-                const TccInfo &inf = s_info[b];
+                const TccInfo &inf = s_info[rs];
                 if (inf.tile < 0) break;
                 const int A = inf.A, N = inf.N, nch = inf.nch;
                 const uint32_t ab = sbase + L.aop + (uint32_t)(b * kCRows * KA * 4);
                 const float *bsrc = p.Bc + (int64_t)A * p.tcc_nch * kCNC * KA;
-                auto load_b = [&](uint32_t gg, int ch) {  // chunk ch of A's list -> slot gg & 1
-                    const int j = gg & 1;
-                    if (gg >= 2) tc::mbar_wait(bempty[j], ((gg - 2) >> 1) & 1);
-                    tc::mbar_arrive_tx(bfull[j], kBBytes);
-                    tc::bulk_g2s(sbase + L.bop + j * kBBytes, bsrc + (int64_t)ch * kCNC * KA, kBBytes, bfull[j]);
+                auto load_b = [&](int ch) {   // fill #nfill[j] of slot j = ch & 1 with chunk ch of A's list
+                    const int j = ch & 1, want = (A << 8) | ch;
+                    // the slot's previous use done (waited for every use, in order: a skipped wait
+                    // would let the phase parity alias two uses later)
+                    if (nfill[j] >= 1) tc::mbar_wait(bempty[j], (uint32_t)((nfill[j] - 1) & 1));
+                    if (tag[j] == want) {
+                        tc::mbar_arrive(bfull[j]);               // still there: an empty fill
+                    } else {
+                        tc::mbar_arrive_tx(bfull[j], kBBytes);
+                        tc::bulk_g2s(sbase + L.bop + j * kBBytes, bsrc + (int64_t)ch * kCNC * KA, kBBytes, bfull[j]);
+                        tag[j] = want;
+                    }
+                    ++nfill[j];
                 };
-                if (nch > 0) load_b(g, 0);
+                if (nch > 0) load_b(0);
                 for (int ch = 0; ch < nch; ++ch, ++g) {
-                    const int j = g & 1;
-                    if (ch + 1 < nch) load_b(g + 1, ch + 1);   // next chunk's copy overlaps these MMAs
-                    tc::mbar_wait(bfull[j], (g >> 1) & 1);
-                    if (g >= 2) tc::mbar_wait(tfree[j], ((g - 2) >> 1) & 1);
+                    const int j = ch & 1, jt = g % kTB;
+                    const int f = nfill[j] - 1;                  // this chunk's fill of slot j
+                    if (ch + 1 < nch) load_b(ch + 1);            // next chunk's copy overlaps these MMAs
+                    tc::mbar_wait(bfull[j], (uint32_t)(f & 1));
+                    if (g >= kTB) tc::mbar_wait(tc::smem_u32(&s_tfree[jt]), ((g / kTB) - 1) & 1);
                     tc::fence_after();
                     const int w = min(kCNC, N - ch * kCNC);
                     const uint32_t idesc = idesc_base | ((uint32_t)(w >> 3) << 17);
                     const uint32_t bb = sbase + L.bop + j * kBBytes;
-                    const uint32_t d = s_tmem + (uint32_t)(j * kCNC);
+                    const uint32_t d = s_tmem + (uint32_t)(jt * kCNC);
 #pragma unroll
                     for (int kb = 0; kb < DP / 8; ++kb)       // x'hi . c'hi
                         tc::mma_tf32(d, tc::sdesc(ab + kb * kCRows * 32), tc::sdesc(bb + kb * kCNC * 32), idesc, kb > 0);
@@ -273,32 +301,38 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
                     for (int kb = 0; kb < DP / 8; ++kb)       // x'hi . c'lo
                         tc::mma_tf32(d, tc::sdesc(ab + kb * kCRows * 32), tc::sdesc(bb + (DP / 8 + kb) * kCNC * 32), idesc, 1);
                     tc::mma_tf32(d, tc::sdesc(ab + (DP / 4) * kCRows * 32), tc::sdesc(bb + (DP / 4) * kCNC * 32), idesc, 1);
-                    tc::mma_commit(tfull[j]);
+                    tc::mma_commit(tc::smem_u32(&s_tfull[jt]));
                     tc::mma_commit(bempty[j]);
                 }
+                tc::mma_commit(tc::smem_u32(&s_afree[b]));   // A slot b free once these MMAs are done
             }
         }
-    } else if (warp < kCPrepW) {
+    } else if (warp < kCPrepW || warp >= kCPrepW1) {
         // ================= prep: bounds, clause 1, tightening, prefix, A operand ============
+        // two groups of 4 warps on alternate tiles (group pg: ring stage pg, A slot pg, H-row
+        // slot pg), so one group's dependent loads overlap the other's
+        const int pg = warp < kCPrepW ? 0 : 1;
+        const int pt = t - (pg ? kCPrepW1 * 32 : 0);    // row in the tile
+        const int pwarp = pt >> 5;
         const float eps = *p.eps;
         const int ncols = k - 1;
         CRow<CSMEM> Cn;
         if constexpr (CSMEM) Cn.base = tc::smem_u32(sC); else Cn.base = p.Cneg;
-        int mA[2] = {-1, -1};
-        uint32_t mpar[2] = {0u, 0u};
-        int mcur = 0;
+        int mA = -1;
+        uint32_t mpar = 0u;
         unsigned long long c_clause1 = 0;
-        for (int i = 0;; ++i) {
-            const int s = i % kCStages, b = i & 1;
+        for (int i = pg;; i += kCStages) {
+            const int s = i % kCStages, b = i & 1, rs = i % kRS;
             tc::mbar_wait(tc::smem_u32(&s_full[s]), (uint32_t)((i / kCStages) & 1));
             const long long tile = s_meta[s];
-            // A buffer, row state and info of slot b are free once the epilogue of tile i - 2 is
-            // done (it waited for every chunk's MMAs of that tile)
-            if (i >= 2) tc::mbar_wait(tc::smem_u32(&s_efree[b]), (uint32_t)(((i - 2) >> 1) & 1));
+            // A slot b is free once the MMAs of tile i - 2 are done; row state and info slot rs
+            // once the epilogue of tile i - kRS is
+            if (i >= 2) tc::mbar_wait(tc::smem_u32(&s_afree[b]), (uint32_t)(((i - 2) >> 1) & 1));
+            if (i >= kRS) tc::mbar_wait(tc::smem_u32(&s_efree[rs]), (uint32_t)(((i / kRS) - 1) & 1));
             if (tile < 0) {
-                if (t == 0) s_info[b].tile = -1;
+                if (pt == 0) s_info[rs].tile = -1;
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[b]));
+                if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[rs]));
                 break;
             }
             const uint8_t *stage = smem + L.ring + s * L.stage_bytes;
@@ -307,34 +341,30 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
             const float *su = reinterpret_cast<const float *>(stage + kCRows * XS + kCRows * 4);
             const int vrows = (int)(n - tile * kCRows < kCRows ? n - tile * kCRows : kCRows);
             const int A = sa[vrows >> 1];
-            int ms;
-            if (mA[mcur] == A) ms = mcur;
-            else if (mA[mcur ^ 1] == A) ms = mcur ^ 1;
-            else {
-                ms = mcur ^ 1;   // every prep thread finished the tiles that read this slot
-                if (t == 0) {
+            const int ms = pg;
+            if (mA != A) {   // every thread of the group finished the tile that read this slot
+                if (pt == 0) {
                     const uint32_t mb = tc::smem_u32(&s_mbar[ms]);
                     const uint32_t hb = (uint32_t)(((HS * 4) + 15) & ~15);
                     tc::mbar_arrive_tx(mb, hb);
                     tc::bulk_g2s(sbase + L.meta + (uint32_t)(ms * hb), p.Mh + (int64_t)A * (hb / 4), hb, mb);
                 }
-                tc::mbar_wait(tc::smem_u32(&s_mbar[ms]), mpar[ms]);
-                mpar[ms] ^= 1u;
-                mA[ms] = A;
+                tc::mbar_wait(tc::smem_u32(&s_mbar[ms]), mpar);
+                mpar ^= 1u;
+                mA = A;
             }
-            mcur = ms;
             const float *meta = meta0 + ms * ((((HS * 4) + 15) & ~15) / 4);
 
-            const int64_t row = tile * kCRows + t;
+            const int64_t row = tile * kCRows + pt;
             const bool valid = row < n;
             float x[DP];
 #pragma unroll
             for (int j = 0; j < DP; j += 4) {
-                const float4 v = lds128(sxa + tcc_swz((uint32_t)(t * XS + j * 4), tcc_swz_mask(DP)));
+                const float4 v = lds128(sxa + tcc_swz((uint32_t)(pt * XS + j * 4), tcc_swz_mask(DP)));
                 x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
             }
-            const int aold = valid ? sa[t] : 0;
-            const float uu = valid ? __fadd_ru(su[t], sF[aold]) : 0.f;       // u += f(a)
+            const int aold = valid ? sa[pt] : 0;
+            const float uu = valid ? __fadd_ru(su[pt], sF[aold]) : 0.f;       // u += f(a)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_sfree[s]));     // the stage is read
             const bool c1 = valid && uu <= sS[aold];                           // clause 1
@@ -380,30 +410,30 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
                         h[q] = __uint_as_float(__float_as_uint(xh[j + q]) & 0xFFFFE000u);
                         l[q] = xh[j + q] - h[q];
                     }
-                    tc::sts128(abuf + tc::op_off(t, j, kCRows), h[0], h[1], h[2], h[3]);
-                    tc::sts128(abuf + tc::op_off(t, DP + j, kCRows), l[0], l[1], l[2], l[3]);
+                    tc::sts128(abuf + tc::op_off(pt, j, kCRows), h[0], h[1], h[2], h[3]);
+                    tc::sts128(abuf + tc::op_off(pt, DP + j, kCRows), l[0], l[1], l[2], l[3]);
                 }
                 const float xxh = __uint_as_float(__float_as_uint(xx) & 0xFFFFE000u);
-                tc::sts128(abuf + tc::op_off(t, 2 * DP, kCRows), xxh, xx - xxh, 1.f, 1.f);
+                tc::sts128(abuf + tc::op_off(pt, 2 * DP, kCRows), xxh, xx - xxh, 1.f, 1.f);
             }
-            row_store(rstate, b, t, st);
+            row_store(rstate, rs, pt, st);
             const int pw = (__reduce_max_sync(kFull, active ? st.p : 0) + 15) & ~15;
             if (lane == 0) {
-                s_info[b].pw[warp] = pw;
-                s_info[b].cm[warp] = pw > 0 ? __ldg(p.Mx + (int64_t)A * NMETA + pw - 1) : 0.f;
+                s_info[rs].pw[pwarp] = pw;
+                s_info[rs].cm[pwarp] = pw > 0 ? __ldg(p.Mx + (int64_t)A * NMETA + pw - 1) : 0.f;
             }
             tc::fence_async_smem();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (t == 0) {
-                TccInfo &inf = s_info[b];
+            asm volatile("bar.sync %0, 128;" :: "r"(1 + pg) : "memory");
+            if (pt == 0) {
+                TccInfo &inf = s_info[rs];
                 inf.tile = tile;
                 inf.A = A;
                 inf.N = max(max(inf.pw[0], inf.pw[1]), max(inf.pw[2], inf.pw[3]));
                 inf.nch = (inf.N + kCNC - 1) / kCNC;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync %0, 128;" :: "r"(1 + pg) : "memory");
             tc::fence_before();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[b]));
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_aready[rs]));
         }
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) c_clause1 += __shfl_xor_sync(kFull, c_clause1, o);
@@ -419,18 +449,18 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
         unsigned long long c_dists = 0, c_cols = 0, c_queued = 0;
         uint32_t g = 0;
         for (int i = 0;; ++i) {
-            const int b = i & 1;
-            tc::mbar_wait(tc::smem_u32(&s_aready[b]), (uint32_t)((i >> 1) & 1));
+            const int rs = i % kRS;
+            tc::mbar_wait(tc::smem_u32(&s_aready[rs]), (uint32_t)((i / kRS) & 1));
             tc::fence_after();
-            const TccInfo inf = s_info[b];
+            const TccInfo inf = s_info[rs];
             if (inf.tile < 0) break;
-            const TccRow st = row_load(rstate, b, r);
+            const TccRow st = row_load(rstate, rs, r);
             const bool valid = st.flags & 1, active = st.flags & 2, misfit = st.flags & 4;
             const int pw = inf.pw[ew];
-            float m = INFINITY;
+            float m = INFINITY, m2 = INFINITY;
             for (int ch = 0; ch < inf.nch; ++ch, ++g) {
-                const int j = g & 1;
-                tc::mbar_wait(tc::smem_u32(&s_tfull[j]), (g >> 1) & 1);
+                const int j = g % kTB;
+                tc::mbar_wait(tc::smem_u32(&s_tfull[j]), (g / kTB) & 1);
                 tc::fence_after();
                 const int c0 = ch * kCNC;
                 const int cend = min(kCNC, pw - c0);
@@ -450,12 +480,16 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
                             if (base + q == st.own) rr[q] = 0x7f800000u;   // the own cluster is no rival
                     }
 #pragma unroll
-                    for (int q = 0; q < 32; q += 2) m = tcc_fmin3(m, __uint_as_float(rr[q]), __uint_as_float(rr[q + 1]));
+                    for (int q = 0; q < 32; q += 4) {      // two independent min chains
+                        m = tcc_fmin3(m, __uint_as_float(rr[q]), __uint_as_float(rr[q + 1]));
+                        m2 = tcc_fmin3(m2, __uint_as_float(rr[q + 2]), __uint_as_float(rr[q + 3]));
+                    }
                 }
                 tc::fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_tfree[j]));
             }
+            m = fminf(m, m2);
             if (lane == 0) c_cols += (unsigned long long)pw;
             bool decided = false;
             if (active) {
@@ -480,7 +514,7 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
             c_queued += qd;
             if (valid) p.u[tile * kCRows + r] = decided ? st.ut : st.uu;
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_efree[b]));
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_efree[rs]));
         }
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) {
@@ -497,7 +531,7 @@ k_tcc(AssignParams p, TccCfg L, const __grid_constant__ CUtensorMap tmap)
     tc::fence_before();
     __syncthreads();
     if (warp == kCMmaW)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(s_tmem), "r"(2 * kCNC));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(s_tmem), "r"(kTB * kCNC));
 }
 
 // S1 (tensor-chunked part): per cluster c, the B operand chunks and column metadata of its

@@ -18,7 +18,9 @@ want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
         "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_lgds.avg",
         "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_shared.avg",
-        "derived__memory_l1_wavefronts_shared_excessive", "sm__cycles_elapsed.avg"]
+        "derived__memory_l1_wavefronts_shared_excessive", "sm__cycles_elapsed.avg",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]
 out = {}
 for i, n in enumerate(h):
     if n in want:
