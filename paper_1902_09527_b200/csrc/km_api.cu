@@ -170,7 +170,6 @@ struct km_ctx {
     int *empty = nullptr, *work = nullptr;
     unsigned *eps_bits = nullptr;
     double *sse_buf = nullptr;
-    int32_t *a_out = nullptr;
     double *exact_P = nullptr;      // exact-order sums: per 64 Ki-row block x cluster partials (B12)
     bool perm_identity = true;      // stored rows still in caller order (no re-bucketing yet)
     HostStat *hstat = nullptr;
@@ -571,7 +570,7 @@ void free_all(km_ctx *c)
     }
     cudaFree(c->keys); cudaFree(c->hist); cudaFree(c->totals); cudaFree(c->base); cudaFree(c->lohist); cudaFree(c->qmap);
     cudaFree(c->C); cudaFree(c->Cprev); cudaFree(c->Cneg); cudaFree(c->f); cudaFree(c->s);
-    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->a_out); cudaFree(c->exact_P); cudaFree(c->qrow); cudaFree(c->qcnt); cudaFree(c->nlrank); cudaFree(c->Bc); cudaFree(c->Mh); cudaFree(c->Mx);
+    cudaFree(c->NL); cudaFree(c->Bop); cudaFree(c->Bmeta); cudaFree(c->defer); cudaFree(c->dcount); cudaFree(c->Wblk); cudaFree(c->WH); cudaFree(c->Wcc); cudaFree(c->Wmeta); cudaFree(c->scratch); cudaFree(c->sse_buf); cudaFree(c->exact_P); cudaFree(c->qrow); cudaFree(c->qcnt); cudaFree(c->nlrank); cudaFree(c->Bc); cudaFree(c->Mh); cudaFree(c->Mx);
     cudaFree(c->counters_g); cudaFree(c->S); cudaFree(c->acc_part); cudaFree(c->L); cudaFree(c->Hm);
     if (c->hstat) cudaFreeHost(c->hstat);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -957,10 +956,12 @@ km_status kmeans_get_assignments(km_ctx *c, int32_t *out, int32_t out_is_device)
     if (!c || !out) return fail(KM_EARG, "NULL argument");
     if (c->t == 0) return fail(KM_ESTATE, "no assignment pass has run yet");
     KM_CUDA(cudaSetDevice(c->device));
-    if (!c->a_out) KM_TRY(dalloc(&c->a_out, (size_t)c->n));
-    KM_CUDA(km::launch_unpermute(c->a[c->cur], c->perm[c->cur], c->n, c->a_out, c->st));
+    // scratch: the idle row buffer's a (dead until the next re-bucketing overwrites it whole); no
+    // allocation on the read-back path (a lazy cudaMalloc here cost 5-30 ms of the e2e run)
+    int32_t *tmp = c->a[1 - c->cur];
+    KM_CUDA(km::launch_unpermute(c->a[c->cur], c->perm[c->cur], c->n, tmp, c->st));
     c->launches += 1;
-    KM_CUDA(cudaMemcpyAsync(out, c->a_out, (size_t)c->n * sizeof(int32_t),
+    KM_CUDA(cudaMemcpyAsync(out, tmp, (size_t)c->n * sizeof(int32_t),
                             out_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
     KM_CUDA(cudaStreamSynchronize(c->st));
     return KM_OK;
@@ -973,12 +974,12 @@ km_status kmeans_get_bounds(km_ctx *c, float *out, int32_t out_is_device)
     if (c->t == 0) return fail(KM_ESTATE, "no assignment pass has run yet");
     if (c->prune == KM_PRUNE_NONE) return fail(KM_ESTATE, "no bounds are kept with KM_PRUNE_NONE");
     KM_CUDA(cudaSetDevice(c->device));
-    if (!c->a_out) KM_TRY(dalloc(&c->a_out, (size_t)c->n));
     // u is 4-byte data in the context's row order: the int32 unpermute moves its bits
-    KM_CUDA(km::launch_unpermute(reinterpret_cast<const int32_t *>(c->u[c->cur]), c->perm[c->cur], c->n, c->a_out,
+    int32_t *tmp = c->a[1 - c->cur];
+    KM_CUDA(km::launch_unpermute(reinterpret_cast<const int32_t *>(c->u[c->cur]), c->perm[c->cur], c->n, tmp,
                                  c->st));
     c->launches += 1;
-    KM_CUDA(cudaMemcpyAsync(out, c->a_out, (size_t)c->n * sizeof(float),
+    KM_CUDA(cudaMemcpyAsync(out, tmp, (size_t)c->n * sizeof(float),
                             out_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
     KM_CUDA(cudaStreamSynchronize(c->st));
     return KM_OK;

@@ -146,8 +146,11 @@ __host__ __device__ constexpr int walk_threads_of(int DP)
 }
 template <int DP> constexpr int walk_threads() { return walk_threads_of(DP); }
 // rows per lane: 2 where the registers allow (the candidate loads are shared by both rows)
-template <int DP> constexpr int walk_r() { return DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1); }
-static inline int walk_r_rt(int DP) { return DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1); }
+#ifndef KM_WALK_R8
+#define KM_WALK_R8 2            // rows per lane at d <= 8
+#endif
+template <int DP> constexpr int walk_r() { return DP <= 8 ? KM_WALK_R8 : (DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1)); }
+static inline int walk_r_rt(int DP) { return DP <= 8 ? KM_WALK_R8 : (DP <= 16 ? 2 : (DP <= 32 ? KM_WALK_R32 : 1)); }
 // d = 32 with the H rows in global memory (large k, C5): three rows per lane at 256 threads per
 // CTA — each candidate pair block a warp loads (256 B, delivered to all 32 lanes through the L1
 // data pipe) then serves 96 rows; measured on C5: 28.0 -> 24.4 ms per pass; on C4 (H rows in
