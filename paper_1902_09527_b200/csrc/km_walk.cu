@@ -99,7 +99,8 @@ size_t walk_smem(int DP, bool csmem, int k, int whs, bool wh_smem, bool skip1)
     const int R = walk_r_sel(DP, wh_smem);
     const int k4 = (k + 3) & ~3;
     return (size_t)((csmem ? k * DP : 0) + 2 * k4 + (wh_smem ? k * whs : 0)) * sizeof(float) +
-           (size_t)(walk_threads_dr(DP, R) / 32) * walk_warp_floats(DP, R, skip1 ? 1 : 0) * sizeof(float);
+           (size_t)(walk_threads_dr(DP, R) / 32) *
+               (walk_warp_floats(DP, R, skip1 ? 1 : 0) + walk_tab_floats(DP, wh_smem, skip1 ? 1 : 0)) * sizeof(float);
 }
 
 
@@ -146,6 +147,12 @@ static walk_kernel_t walk_pick(int whs, bool hs, bool skip1)
 static walk_kernel_t walk_kernel(int DP, bool csmem, int whs, bool hs, bool skip1)
 {
     switch (DP * 2 + (csmem ? 1 : 0)) {
+#ifdef KM_WALK_FAST_BUILD      // A/B variant builds: only the row widths of C3 and C4 / C5
+    case 17: return walk_pick<8, true>(whs, hs, skip1);
+    case 64: return walk_pick<32, false>(whs, hs, skip1);
+    case 65: return walk_pick<32, true>(whs, hs, skip1);
+    default: return nullptr;
+#else
     case 8: return walk_pick<4, false>(whs, hs, skip1);
     case 9: return walk_pick<4, true>(whs, hs, skip1);
     case 16: return walk_pick<8, false>(whs, hs, skip1);
@@ -156,6 +163,7 @@ static walk_kernel_t walk_kernel(int DP, bool csmem, int whs, bool hs, bool skip
     case 65: return walk_pick<32, true>(whs, hs, skip1);
     case 128: return walk_pick<64, false>(whs, hs, skip1);
     case 129: return walk_pick<64, true>(whs, hs, skip1);
+#endif
     }
     return nullptr;
 }

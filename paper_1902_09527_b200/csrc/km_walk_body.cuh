@@ -18,7 +18,12 @@ KM_WALK_NAME(AssignParams p)
     float *sH = sS + k4;                            // k x NH H rows (HSMEM)
     // per-warp staging of the next batch (cp.async): x rows, then a, then u
     constexpr int kRowsB = 32 * R;
-    float *stg = sH + (HSMEM ? k * NH : 0) + (threadIdx.x >> 5) * walk_warp_floats(DP, R, KM_SKIP1);
+    constexpr int kTab = walk_tab_cap(DP, HSMEM, KM_SKIP1);   // candidates of A's list kept in shared memory
+    float *stg = sH + (HSMEM ? k * NH : 0) +
+                 (threadIdx.x >> 5) * (walk_warp_floats(DP, R, KM_SKIP1) + walk_tab_floats(DP, HSMEM, KM_SKIP1));
+    float *tabB = stg + walk_warp_floats(DP, R, KM_SKIP1);   // kTab / 2 pair blocks (2 DP floats each)
+    float *tabC = tabB + kTab * DP;                           // |c'|^2 of the kTab candidates
+    int tabA = -1;                                            // cluster whose table head is in tabB / tabC
 #if KM_SKIP1
     // a second [a | u] slot: the a/u of the batch after the one whose rows are staged
     float *sAU2 = stg + kRowsB * (DP + 2) + 3 * kQueue;
@@ -254,33 +259,8 @@ KM_WALK_NAME(AssignParams p)
             amask |= __ballot_sync(kFull, active[i]) ? (1u << i) : 0u;
         }
         __syncwarp();
-#if KM_SKIP1
-        // rows of b1 that fail clause 1 (their a/u are here), a/u of b2 into b0's slot
-        b2 = b1 < n ? next_batch() : n;
-        stage_x_live(b1, slot ^ 1);
-        stage_au(b2, slot);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        b0 = b1;
-        b1 = b2;
-        slot ^= 1;
-        chunk_row = b0;                             // loop condition
-#else
-        if (++bt == kBatches || chunk_row + bt * kRows >= n) {
-            bt = 0;
-            const int c = __shfl_sync(kFull, ahead_c, 0);
-            chunk_row = c < nchunks ? c * kChunk : n;
-            if (lane == 0 && chunk_row < n) ahead_c = atomicAdd(p.work, 1);
-        }
-        if (chunk_row < n) stage(chunk_row + bt * kRows);
-#endif
-
-        int anew[R];
-        float unew[R], ut[R];
-        bool defer[R];
-#pragma unroll
-        for (int i = 0; i < R; ++i) { anew[i] = aold[i]; unew[i] = uu[i]; ut[i] = 0.f; defer[i] = false; }
-        if (amask) {
-            // warp cluster A: the middle row's if active, else the first active row's
+        // warp cluster A: the middle row's if active, else the first active row's
+        auto pickA = [&]() -> int {
             int A;
             if constexpr (R <= 2) {
                 const int mid = R == 1 ? 16 : 0;            // R = 2: lane 0 of the second half
@@ -306,6 +286,58 @@ KM_WALK_NAME(AssignParams p)
                     A = __shfl_sync(kFull, av, fl);
                 }
             }
+            return A;
+        };
+#if KM_WALK_TAB
+        // chosen before the next batch is staged, so that the table copy's group precedes the rows'
+        int A = 0;
+        if (amask) A = pickA();
+#endif
+        [[maybe_unused]] bool staged_next = false;
+#if KM_WALK_TAB
+        if constexpr (kTab > 0) {
+            // head of A's candidate table -> this warp's shared-memory copy (its own cp.async group,
+            // committed before the next batch's rows so that the walk waits for it alone)
+            if (amask && A != tabA) {
+                tabA = A;
+                const int capn = min(kTab, kp);
+                const float4 *src = p.Wblk + (int64_t)A * (kp / 2) * walk_pair_f4(DP);
+                float4 *dst = reinterpret_cast<float4 *>(tabB);
+                for (int c = lane; c < (capn / 2) * (DP / 2); c += 32) cp_async16(dst + c, src + c);
+                if (lane < capn / 2) cp_async8(tabC + 2 * lane, p.Wcc + (int64_t)A * kp + 2 * lane);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+#endif
+#if KM_SKIP1
+        // rows of b1 that fail clause 1 (their a/u are here), a/u of b2 into b0's slot
+        b2 = b1 < n ? next_batch() : n;
+        stage_x_live(b1, slot ^ 1);
+        stage_au(b2, slot);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        b0 = b1;
+        b1 = b2;
+        slot ^= 1;
+        chunk_row = b0;                             // loop condition
+#else
+        if (++bt == kBatches || chunk_row + bt * kRows >= n) {
+            bt = 0;
+            const int c = __shfl_sync(kFull, ahead_c, 0);
+            chunk_row = c < nchunks ? c * kChunk : n;
+            if (lane == 0 && chunk_row < n) ahead_c = atomicAdd(p.work, 1);
+        }
+        if (chunk_row < n) { stage(chunk_row + bt * kRows); staged_next = true; }
+#endif
+
+        int anew[R];
+        float unew[R], ut[R];
+        bool defer[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) { anew[i] = aold[i]; unew[i] = uu[i]; ut[i] = 0.f; defer[i] = false; }
+        if (amask) {
+#if !KM_WALK_TAB
+            const int A = pickA();
+#endif
             float4 cA[DP / 4];
 #pragma unroll
             for (int j = 0; j < DP / 4; ++j) cA[j] = Cn.ld(A, DP, 4 * j);
@@ -356,8 +388,14 @@ KM_WALK_NAME(AssignParams p)
             int m1[R], m2[R];
 #pragma unroll
             for (int i = 0; i < R; ++i) { m1[i] = 0x7fffffff; m2[i] = 0x7fffffff; }
-            for (int j = 0; j < pm; j += 2) {
-                const float2 cc = __ldg(ccA + (j >> 1));
+            // one step: candidates (j, j + 1); TB: from this warp's shared-memory table head
+            auto step = [&](const int j, auto TBt) {
+                constexpr bool TB = decltype(TBt)::value;
+                const float4 *tb4 = reinterpret_cast<const float4 *>(tabB) + (j >> 1) * (DP / 2);
+                const float4 *gb4 = blk + (int64_t)(j >> 1) * walk_pair_f4(DP);
+                float2 cc;
+                if constexpr (TB) cc = reinterpret_cast<const float2 *>(tabC)[j >> 1];
+                else cc = __ldg(ccA + (j >> 1));
                 float2 q[R];
                 if constexpr (DP >= 32 && KM_WALK_HALVES && HSMEM) {   // (measured: +2 % on C4, -3.5 % on C5)
                     // wide rows: the pair block is consumed in two halves of DP/2 coordinates, so
@@ -368,8 +406,10 @@ KM_WALK_NAME(AssignParams p)
                     for (int h = 0; h < 2; ++h) {
                         float4 v[DP / 4];
 #pragma unroll
-                        for (int e = 0; e < DP / 4; e += 2)
-                            ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + h * (DP / 4) + e, v[e], v[e + 1]);
+                        for (int e = 0; e < DP / 4; e += 2) {
+                            if constexpr (TB) { v[e] = tb4[h * (DP / 4) + e]; v[e + 1] = tb4[h * (DP / 4) + e + 1]; }
+                            else ldg256(gb4 + h * (DP / 4) + e, v[e], v[e + 1]);
+                        }
 #pragma unroll
                         for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -381,8 +421,10 @@ KM_WALK_NAME(AssignParams p)
                 } else {
                     float4 v[DP / 2];
 #pragma unroll
-                    for (int e = 0; e < DP / 2; e += 2)      // 32-byte loads: half the L1 requests
-                        ldg256(blk + (int64_t)(j >> 1) * walk_pair_f4(DP) + e, v[e], v[e + 1]);
+                    for (int e = 0; e < DP / 2; e += 2) {    // 32-byte loads: half the L1 requests
+                        if constexpr (TB) { v[e] = tb4[e]; v[e + 1] = tb4[e + 1]; }
+                        else ldg256(gb4 + e, v[e], v[e + 1]);
+                    }
 #pragma unroll
                     for (int i = 0; i < R; ++i) q[i] = q_pair<DP>(xc[i], xx[i], cc, v);
                 }
@@ -395,6 +437,18 @@ KM_WALK_NAME(AssignParams p)
                     m2[i] = min(min(max(m1[i], lo2), m2[i]), hi2);
                     m1[i] = min(m1[i], lo2);
                 }
+            };
+            {
+                int j = 0;
+                if constexpr (kTab > 0) {
+                    // the table head of A landed (its group precedes the next batch's rows)
+                    if (staged_next) asm volatile("cp.async.wait_group 1;" ::: "memory");
+                    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+                    __syncwarp();
+                    const int je = min(pm, min(kTab, kp));
+                    for (; j < je; j += 2) step(j, km_true{});
+                }
+                for (; j < pm; j += 2) step(j, km_false{});
             }
             steps32 += (unsigned)pm;
             const float2 *mA = p.Wmeta + (int64_t)A * kp;

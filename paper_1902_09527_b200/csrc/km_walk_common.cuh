@@ -18,6 +18,8 @@ namespace km {
 #ifndef KM_WALK_CHUNK
 #define KM_WALK_CHUNK 128       // measured: 64 1.73 ms, 128 1.67, 256 1.69, 512 1.73, 1024 1.80 (C3)
 #endif
+struct km_true { static constexpr bool value = true; };
+struct km_false { static constexpr bool value = false; };
 constexpr int kWalkChunk = KM_WALK_CHUNK;   // rows a warp claims per work-counter fetch
 constexpr int kQueue = 64;             // mover-queue entries per warp (< 32 left + 32 new)
 
@@ -29,6 +31,25 @@ __host__ __device__ constexpr int walk_warp_floats(int DP, int R, int skip1)
 }
 
 __host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // float4 per candidate pair
+
+// Per-warp shared-memory copy of the head of the warp cluster's candidate table (KM_WALK_TAB 1):
+// the first walk_tab_cap candidates of A's list (pair blocks + |c'|^2) are copied once per change
+// of A with cp.async (a group of its own, committed before the next batch's rows) and then read
+// with broadcast LDS instead of broadcast LDG: 5.0 against 8.2 SM cycles per 32-B block per warp
+// (tools/probes/ldc_probe.cu), and no L1 miss on the walk's dependent path — at d = 32 the
+// tables (k^2 x 132 B = 1.3 MB at k = 100) do not fit L1 and the walk runs 3 warps per
+// sub-partition, so every miss showed as a long-scoreboard stall.  Measured: C4 6.28 -> 5.56 ms
+// per pass; C3 (d = 8) 1.565 -> 1.559 ms, so only d = 32 takes it.  Only with the H rows in
+// shared memory and without SKIP1.  Shared memory at d = 32: <= 186,240 B without the table for
+// every k that keeps the H rows in shared memory (k <= 112), + 12 warps x 24 x 132 B = 224,256 B.
+#ifndef KM_WALK_TAB
+#define KM_WALK_TAB 1
+#endif
+__host__ __device__ constexpr int walk_tab_cap(int DP, bool hs, int skip1)
+{
+    return (KM_WALK_TAB && hs && !skip1 && DP == 32) ? 24 : 0;
+}
+__host__ __device__ constexpr int walk_tab_floats(int DP, bool hs, int skip1) { return walk_tab_cap(DP, hs, skip1) * (DP + 1); }
 
 // 32-byte read-only load (LDG.E.ENL2.256): two float4 in one instruction
 __device__ __forceinline__ void ldg256(const float4 *src, float4 &a, float4 &b)
@@ -108,6 +129,11 @@ __device__ __forceinline__ int count_below_s(const float *h, float T)
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
     return (int)((a - a0) >> 2) + (v < T ? 1 : 0);
+}
+
+__device__ __forceinline__ void cp_async8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
 }
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src)
