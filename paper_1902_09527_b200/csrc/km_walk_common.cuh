@@ -45,9 +45,12 @@ __host__ __device__ constexpr int walk_pair_f4(int DP) { return DP / 2; }   // f
 #ifndef KM_WALK_TAB
 #define KM_WALK_TAB 1
 #endif
+#ifndef KM_WALK_TAB_CAP
+#define KM_WALK_TAB_CAP 24      // even; 28 is the most that fits beside the H rows at k = 112
+#endif
 __host__ __device__ constexpr int walk_tab_cap(int DP, bool hs, int skip1)
 {
-    return (KM_WALK_TAB && hs && !skip1 && DP == 32) ? 24 : 0;
+    return (KM_WALK_TAB && hs && !skip1 && DP == 32) ? KM_WALK_TAB_CAP : 0;
 }
 __host__ __device__ constexpr int walk_tab_floats(int DP, bool hs, int skip1) { return walk_tab_cap(DP, hs, skip1) * (DP + 1); }
 

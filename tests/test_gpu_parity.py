@@ -166,7 +166,7 @@ def test_c2_lockstep_single_step():
 
 # ---- edge cases ------------------------------------------------------------------------------
 @pytest.mark.parametrize("engine", ["cuda", "screen"])
-@pytest.mark.parametrize("d", [1, 2, 3, 5, 12, 33, 64])
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 12, 20, 32, 33, 64])
 def test_dims_padding(d, engine):
     rng = np.random.default_rng(d)
     X = (rng.normal(size=(3001, d)) + rng.integers(0, 4, size=(3001, 1)) * 3).astype(np.float32)
@@ -174,6 +174,21 @@ def test_dims_padding(d, engine):
     r = oracle.lloyd(X, C0, 60, 0, "brute")
     for prune in ("mti", "none"):
         assert_strict(gpu_run(X, C0, 60, prune, engine=engine), r)
+
+
+@pytest.mark.parametrize("k", [2, 7, 23, 24, 25, 26, 40, 112])
+def test_walk_table_head_boundaries(k):
+    """d = 32 walk with the per-warp shared-memory copy of the first 24 candidates of the warp
+    cluster's list (km_walk_common.cuh, walk_tab_cap): lists shorter than, equal to and longer than
+    the copied head (the tail is read from global memory), overlapping clusters so that walks are
+    long and rows move between clusters for many iterations."""
+    rng = np.random.default_rng(1000 + k)
+    n = 40_003
+    means = rng.uniform(-3, 3, size=(k, 32))
+    X = (means[rng.integers(0, k, size=n)] + rng.normal(size=(n, 32)) * 2.0).astype(np.float32)
+    C0 = X[rng.choice(n, k, replace=False)].astype(float)
+    r = oracle.lloyd(X, C0, 25, 0, "brute")
+    assert_strict(gpu_run(X, C0, 25, "mti", engine="cuda"), r)
 
 
 @pytest.mark.parametrize("engine", ["cuda", "screen", "tensor_screen", "tensor_chunked"])
