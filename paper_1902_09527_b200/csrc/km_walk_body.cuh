@@ -402,6 +402,11 @@ KM_WALK_NAME(AssignParams p)
                     // only DP/4 float4 of it are live at once (registers bound the resident warps)
 #pragma unroll
                     for (int i = 0; i < R; ++i) q[i] = add2s(xx[i], cc);
+#if KM_WALK_CHAINS2
+                    float2 qb[R];
+#pragma unroll
+                    for (int i = 0; i < R; ++i) qb[i] = make_float2(0.f, 0.f);
+#endif
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         float4 v[DP / 4];
@@ -410,6 +415,19 @@ KM_WALK_NAME(AssignParams p)
                             if constexpr (TB) { v[e] = tb4[h * (DP / 4) + e]; v[e + 1] = tb4[h * (DP / 4) + e + 1]; }
                             else ldg256(gb4 + h * (DP / 4) + e, v[e], v[e + 1]);
                         }
+#if KM_WALK_CHAINS2
+                        // two accumulation chains per row (even / odd coordinates): with 3 warps per
+                        // sub-partition the FFMA2 dependency latency is the top stall once the
+                        // candidate loads come from shared memory; the error bound kappa holds for
+                        // any summation order
+#pragma unroll
+                        for (int i = 0; i < R; ++i)
+#pragma unroll
+                            for (int e = 0; e < DP / 4; ++e) {
+                                q[i] = fma2s(xc[i][h * (DP / 2) + 2 * e], make_float2(v[e].x, v[e].y), q[i]);
+                                qb[i] = fma2s(xc[i][h * (DP / 2) + 2 * e + 1], make_float2(v[e].z, v[e].w), qb[i]);
+                            }
+#else
 #pragma unroll
                         for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -417,7 +435,12 @@ KM_WALK_NAME(AssignParams p)
                                 q[i] = fma2s(xc[i][h * (DP / 2) + 2 * e], make_float2(v[e].x, v[e].y), q[i]);
                                 q[i] = fma2s(xc[i][h * (DP / 2) + 2 * e + 1], make_float2(v[e].z, v[e].w), q[i]);
                             }
+#endif
                     }
+#if KM_WALK_CHAINS2
+#pragma unroll
+                    for (int i = 0; i < R; ++i) q[i] = add2(q[i], qb[i]);
+#endif
                 } else {
                     float4 v[DP / 2];
 #pragma unroll

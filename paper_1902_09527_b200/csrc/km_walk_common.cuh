@@ -15,6 +15,9 @@ namespace km {
 #ifndef KM_WALK_HALVES
 #define KM_WALK_HALVES 1        // d >= 32: consume each candidate pair block in two halves
 #endif
+#ifndef KM_WALK_CHAINS2
+#define KM_WALK_CHAINS2 0       // d >= 32 (halves): two FFMA2 accumulation chains per row
+#endif
 #ifndef KM_WALK_CHUNK
 #define KM_WALK_CHUNK 128       // measured: 64 1.73 ms, 128 1.67, 256 1.69, 512 1.73, 1024 1.80 (C3)
 #endif
